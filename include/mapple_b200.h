@@ -1,0 +1,154 @@
+/*
+ * mapple_b200.h -- C ABI of the B200-native Mapple mapping/execution library.
+ *
+ * Plain C types only (no torch, no CUDA headers needed by callers: streams are
+ * passed as `void*` = cudaStream_t/CUstream, device buffers as raw pointers).
+ * Every device buffer is owned by the caller; the library never allocates or
+ * frees caller memory (transient scratch is passed in explicitly).  All
+ * launches are stream-ordered; no entry point synchronises the device except
+ * where documented.  Return value: PM_OK (0) or a PM_ERR_* code with a
+ * thread-local message in pm_last_error().
+ *
+ * Reference interfaces each entry point replaces (paths under the reference
+ * root, pkg/src/procmap/):
+ *   pm_plan_create / pm_plan_destroy
+ *       <- compile_mapper() / MappingFunction (dsl/interp.py:366-433): the
+ *          per-ispace prefix is evaluated on the host and the per-point suffix
+ *          is lowered to a pm_program (paper_2507_17087_b200/dsl/lower.py).
+ *   pm_map_batch
+ *       <- the per-point loop `fn(pt, ispace)` of cmd_map (cli.py:155-161)
+ *          and shard_policy (tasksim/sim.py:78); MappingFunction.__call__
+ *          (dsl/interp.py:401-418) + ProcSpace.resolve (spaces.py:185-213).
+ *   pm_partition
+ *       <- expand_shards / shard_policy ownership leaves (tasksim/sim.py:67-120)
+ *          and proc_counts (cli.py:154-164): a stable partition of points by
+ *          processor.
+ *   pm_halo_lists
+ *       <- oracle_boundary_count (commvol.py:136-168): per-(src,dst) halo
+ *          transfer lists of a block-mapped grid whose totals equal the count.
+ *   pm_gemm_bf16
+ *       <- the per-processor tile product of the paper's matmul workloads
+ *          (PAPER.md:493); no reference code exists.
+ */
+#ifndef MAPPLE_B200_H
+#define MAPPLE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PM_ABI_VERSION 1
+
+/* status codes */
+#define PM_OK 0
+#define PM_ERR_INVALID 1     /* bad argument / malformed program            */
+#define PM_ERR_CUDA 2        /* CUDA runtime or driver failure               */
+#define PM_ERR_NVRTC 3       /* JIT compilation of the point program failed  */
+#define PM_ERR_UNSUPPORTED 4 /* shape / size outside what the kernel handles */
+
+/* point-program opcodes (dsl/lower.py OP_*) */
+enum pm_opcode {
+  PM_OP_CONST = 0,  /* dst = imm (128-bit: lo | hi << 64)                 */
+  PM_OP_COORD = 1,  /* dst = point coordinate `lo`                        */
+  PM_OP_ADD = 2,    /* dst = a + b                                        */
+  PM_OP_SUB = 3,    /* dst = a - b                                        */
+  PM_OP_MUL = 4,    /* dst = a * b                                        */
+  PM_OP_DIV = 5,    /* dst = floor(a / b); c = 1: a >= 0 and b > 0 proven;
+                       site >= 0: fail(site) when b == 0                  */
+  PM_OP_MOD = 6,    /* dst = a - b * floor(a / b); flags as PM_OP_DIV     */
+  PM_OP_GT = 7,     /* dst = a > b                                        */
+  PM_OP_LT = 8,     /* dst = a < b                                        */
+  PM_OP_EQ = 9,     /* dst = a == b                                       */
+  PM_OP_SELECT = 10,/* dst = a ? b : c                                    */
+  PM_OP_MOV = 11,   /* dst = a                                            */
+  PM_OP_CHECK = 12, /* fail(site) unless lo <= a < hi                     */
+  PM_OP_FAIL = 13,  /* fail(site)                                         */
+  PM_OP_IF = 14,    /* if (a != 0) {                                      */
+  PM_OP_ELSE = 15,  /* } else {                                           */
+  PM_OP_ENDIF = 16, /* }                                                  */
+  PM_OP_RET = 17    /* processor id = a                                   */
+};
+
+typedef struct pm_insn {
+  int32_t op, dst, a, b, c, site;
+  int64_t lo, hi;
+} pm_insn;
+
+typedef struct pm_program {
+  int32_t n_insns;
+  const pm_insn* insns;
+  int32_t n_regs;
+  const uint8_t* reg_width; /* per register: 0 = int32, 1 = int64, 2 = int128 */
+  int32_t n_coords;         /* rank of an iteration point                      */
+  int32_t implicit;         /* 1: points are the row-major ispace enumeration  */
+  const int64_t* extents;   /* n_coords ispace extents (implicit mode)         */
+} pm_program;
+
+typedef struct pm_plan pm_plan;
+
+int pm_abi_version(void);
+const char* pm_last_error(void);
+
+/* CUDA C++ source of the specialised point kernel (for inspection/tests).
+ * Writes at most `cap` bytes (NUL-terminated) and the full length to *len. */
+int pm_codegen(const pm_program* prog, char* buf, size_t cap, size_t* len);
+
+/* JIT-compile the point program for the current device (NVRTC, sm_100a) and
+ * load it.  Needs a GPU only for the final module load; with `load == 0` the
+ * program is compiled to a cubin and discarded (a CPU-side build check). */
+int pm_compile_check(const pm_program* prog);
+int pm_plan_create(const pm_program* prog, pm_plan** out);
+void pm_plan_destroy(pm_plan* plan);
+
+/* Map n points.  points: NULL in implicit mode (point i is the row-major
+ * point `first + i` of the ispace) or n * n_coords int32 row-major.
+ * out_proc[i] = node * procs_per_node + proc, or -1 where the point failed.
+ * status (device, 8 bytes, caller initialises to UINT64_MAX): atomicMin of
+ * ((first + i) << 16 | site) over failing points -- the lowest failing index
+ * and the site it failed at. */
+int pm_map_batch(const pm_plan* plan, const int32_t* points, int64_t n, int64_t first,
+                 int32_t* out_proc, uint64_t* status, void* stream);
+
+/* Stable partition of n processor ids in [0, nbins):
+ *   counts[b]  = #points with id b                    (int64, device)
+ *   offsets[b] = exclusive prefix of counts           (int64, device)
+ *   perm[...]  = point indices grouped by id, each group in input order.
+ * ids outside [0, nbins) are an error (PM_ERR_INVALID is reported via
+ * `bad`, a device int64 set to the first offending index, or -1).
+ * scratch: pm_partition_scratch_bytes(n, nbins) bytes of device memory. */
+size_t pm_partition_scratch_bytes(int64_t n, int32_t nbins);
+int pm_partition(const int32_t* proc, int64_t n, int32_t nbins, int64_t* counts,
+                 int64_t* offsets, int32_t* perm, int64_t* bad, void* scratch,
+                 size_t scratch_bytes, void* stream);
+
+/* Halo transfer lists of a 2D/3D grid owned cell-by-cell (owner = int32 proc
+ * id per cell, row-major, extents ext[0..rank-1]).  A cell c of owner P is
+ * sent to Q != P along dim n / direction s when the first cell of a different
+ * owner among c + s*j*e_n (1 <= j <= halo[n]) is owned by Q; one entry per
+ * (cell, dim, direction).  Totals equal oracle_boundary_count for block
+ * partitions.  Output grouped by key = src * nprocs + dst, cells ascending:
+ *   pair_counts[nprocs*nprocs], pair_offsets[nprocs*nprocs] (int64, device),
+ *   cells[...] (int64 linear cell index), dims[...] (int8: 2*n + (s > 0)).
+ * Pass cells == NULL to count only.  scratch: pm_halo_scratch_bytes(). */
+size_t pm_halo_scratch_bytes(const int64_t* ext, int32_t rank, int32_t nprocs);
+int pm_halo_lists(const int32_t* owner, const int64_t* ext, int32_t rank,
+                  const int32_t* halo, int32_t nprocs, int64_t* pair_counts,
+                  int64_t* pair_offsets, int64_t* cells, int8_t* dims, void* scratch,
+                  size_t scratch_bytes, void* stream);
+
+/* C[M,N] (+)= A[M,K] * B[K,N] on the tcgen05 tensor cores, bf16 inputs, fp32
+ * accumulation.  A is row-major (K contiguous, lda >= K); B is given
+ * transposed as Bt[N,K] row-major (K contiguous, ldb >= K).  C is row-major
+ * fp32 (ldc >= N) or bf16 when c_bf16 != 0; accumulate != 0 adds into C.
+ * M, N multiples of 128 and K a multiple of 64 (PM_ERR_UNSUPPORTED otherwise). */
+int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t ldb, void* C,
+                 int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t c_bf16,
+                 int32_t accumulate, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MAPPLE_B200_H */

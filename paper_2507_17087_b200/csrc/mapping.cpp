@@ -1,0 +1,441 @@
+// K1 -- batched mapping evaluation.
+//
+// A pm_program (the lowered per-point suffix of a Mapple mapping function,
+// see paper_2507_17087_b200/dsl/lower.py) is turned into CUDA C++ with every
+// processor-space extent, stride and divisor baked in as an immediate, JIT
+// compiled by NVRTC for sm_100a and launched over the points of an index
+// launch.  Replaces the reference's interpreted per-point loop
+// (dsl/interp.py:401-418 + spaces.py:185-213, driven by cli.py:155-161).
+//
+// The kernel is HBM-bound: each thread maps 4 consecutive points, loads their
+// coordinates with 16-byte vector loads (explicit mode) or derives them from
+// the linear index (implicit row-major mode, 0 input bytes), evaluates the
+// integer program in registers and writes 4 processor ids with one 16-byte
+// store.  Register widths come from the host's interval analysis, so most
+// programs run in 32-bit integer arithmetic with constant divisors.
+
+#include <nvrtc.h>
+
+#include <climits>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "pm_common.h"
+
+namespace pm {
+
+namespace {
+
+const char* kSigned[3] = {"int", "long long", "__int128"};
+const char* kUnsigned[3] = {"unsigned", "unsigned long long", "unsigned __int128"};
+
+const char* kPrelude = R"CUDA(
+template <typename T> __device__ __forceinline__ T pm_fdiv(T a, T b) {
+  T q = a / b; T r = a - q * b;
+  return (r != 0 && ((r < 0) != (b < 0))) ? q - 1 : q;
+}
+template <typename T> __device__ __forceinline__ T pm_fmod(T a, T b) {
+  T r = a % b;
+  return (r != 0 && ((r < 0) != (b < 0))) ? r + b : r;
+}
+#define PM_FAIL(s) do { *site_out = (s); return -1; } while (0)
+)CUDA";
+
+struct Gen {
+  const pm_program* p;
+  std::ostringstream o;
+  int max_w = 0;
+
+  int w(int r) const { return p->reg_width[r]; }
+
+  std::string cst(int width, long long lo, long long hi) {
+    std::ostringstream s;
+    if (width == 2) {
+      s << "((__int128)(((unsigned __int128)(unsigned long long)" << (unsigned long long)hi
+        << "ULL << 64) | (unsigned __int128)(unsigned long long)" << (unsigned long long)lo
+        << "ULL))";
+    } else {
+      s << "((" << kSigned[width] << ")(long long)" << (unsigned long long)lo << "ULL)";
+    }
+    return s.str();
+  }
+
+  int check() {
+    for (int i = 0; i < p->n_regs; ++i) {
+      if (p->reg_width[i] > 2) return set_error("register %d has bad width", i), PM_ERR_INVALID;
+      if (p->reg_width[i] > max_w) max_w = p->reg_width[i];
+    }
+    int depth = 0;
+    bool ret = false;
+    for (int i = 0; i < p->n_insns; ++i) {
+      const pm_insn& in = p->insns[i];
+      auto bad = [&](int r) { return r < 0 || r >= p->n_regs; };
+      switch (in.op) {
+        case PM_OP_CONST: case PM_OP_COORD:
+          if (bad(in.dst)) return set_error("insn %d: bad dst", i), PM_ERR_INVALID;
+          if (in.op == PM_OP_COORD && (in.lo < 0 || in.lo >= p->n_coords))
+            return set_error("insn %d: bad coordinate", i), PM_ERR_INVALID;
+          break;
+        case PM_OP_ADD: case PM_OP_SUB: case PM_OP_MUL: case PM_OP_DIV: case PM_OP_MOD:
+        case PM_OP_GT: case PM_OP_LT: case PM_OP_EQ:
+          if (bad(in.dst) || bad(in.a) || bad(in.b))
+            return set_error("insn %d: bad operand", i), PM_ERR_INVALID;
+          break;
+        case PM_OP_SELECT:
+          if (bad(in.dst) || bad(in.a) || bad(in.b) || bad(in.c))
+            return set_error("insn %d: bad operand", i), PM_ERR_INVALID;
+          break;
+        case PM_OP_MOV:
+          if (bad(in.dst) || bad(in.a)) return set_error("insn %d: bad operand", i), PM_ERR_INVALID;
+          break;
+        case PM_OP_CHECK: case PM_OP_IF: case PM_OP_RET:
+          if (bad(in.a)) return set_error("insn %d: bad operand", i), PM_ERR_INVALID;
+          if (in.op == PM_OP_IF) ++depth;
+          if (in.op == PM_OP_RET) ret = true;
+          break;
+        case PM_OP_FAIL: break;
+        case PM_OP_ELSE: if (depth <= 0) return set_error("insn %d: stray else", i), PM_ERR_INVALID; break;
+        case PM_OP_ENDIF:
+          if (--depth < 0) return set_error("insn %d: stray endif", i), PM_ERR_INVALID;
+          break;
+        default: return set_error("insn %d: unknown opcode %d", i, in.op), PM_ERR_INVALID;
+      }
+      if ((in.op == PM_OP_CHECK || in.op == PM_OP_FAIL ||
+           ((in.op == PM_OP_DIV || in.op == PM_OP_MOD) && in.site >= 0)) &&
+          (in.site < 0 || in.site > 0xFFFF))
+        return set_error("insn %d: bad site %d", i, in.site), PM_ERR_INVALID;
+    }
+    if (depth != 0) return set_error("unbalanced if/endif"), PM_ERR_INVALID;
+    (void)ret;
+    if (p->n_coords < 0 || p->n_coords > 16) return set_error("bad rank"), PM_ERR_INVALID;
+    return PM_OK;
+  }
+
+  void reg(int r) { o << "r" << r; }
+
+  void body() {
+    int ind = 1;
+    auto pad = [&]() { for (int i = 0; i < ind; ++i) o << "  "; };
+    for (int i = 0; i < p->n_insns; ++i) {
+      const pm_insn& in = p->insns[i];
+      if (in.op == PM_OP_ELSE || in.op == PM_OP_ENDIF) --ind;
+      pad();
+      const int d = in.dst;
+      switch (in.op) {
+        case PM_OP_CONST: o << "r" << d << " = " << cst(w(d), in.lo, in.hi) << ";\n"; break;
+        case PM_OP_COORD: o << "r" << d << " = (" << kSigned[w(d)] << ")c" << in.lo << ";\n"; break;
+        case PM_OP_ADD: case PM_OP_SUB: case PM_OP_MUL: {
+          const char* op = in.op == PM_OP_ADD ? "+" : in.op == PM_OP_SUB ? "-" : "*";
+          const char* u = kUnsigned[w(d)];
+          o << "r" << d << " = (" << kSigned[w(d)] << ")((" << u << ")r" << in.a << " " << op
+            << " (" << u << ")r" << in.b << ");\n";
+          break;
+        }
+        case PM_OP_DIV: case PM_OP_MOD: {
+          int cw = std::max(w(d), std::max(w(in.a), w(in.b)));
+          const char* ct = kSigned[cw];
+          const char* ut = kUnsigned[cw];
+          o << "{ " << ct << " x = (" << ct << ")r" << in.a << ", y = (" << ct << ")r" << in.b
+            << "; ";
+          if (in.site >= 0) o << "if (y == 0) PM_FAIL(" << in.site << "); ";
+          if (in.c & 1) {
+            o << "r" << d << " = (" << kSigned[w(d)] << ")((" << ut << ")x "
+              << (in.op == PM_OP_DIV ? "/" : "%") << " (" << ut << ")y); }\n";
+          } else {
+            o << "r" << d << " = (" << kSigned[w(d)] << ")"
+              << (in.op == PM_OP_DIV ? "pm_fdiv" : "pm_fmod") << "(x, y); }\n";
+          }
+          break;
+        }
+        case PM_OP_GT: case PM_OP_LT: case PM_OP_EQ: {
+          int cw = std::max(w(in.a), w(in.b));
+          const char* op = in.op == PM_OP_GT ? ">" : in.op == PM_OP_LT ? "<" : "==";
+          o << "r" << d << " = ((" << kSigned[cw] << ")r" << in.a << " " << op << " ("
+            << kSigned[cw] << ")r" << in.b << ") ? 1 : 0;\n";
+          break;
+        }
+        case PM_OP_SELECT:
+          o << "r" << d << " = r" << in.a << " ? (" << kSigned[w(d)] << ")r" << in.b << " : ("
+            << kSigned[w(d)] << ")r" << in.c << ";\n";
+          break;
+        case PM_OP_MOV: o << "r" << d << " = (" << kSigned[w(d)] << ")r" << in.a << ";\n"; break;
+        case PM_OP_CHECK: {
+          int cw = std::max(w(in.a), (in.lo < INT_MIN || in.hi > INT_MAX) ? 1 : 0);
+          const char* ct = kSigned[cw];
+          o << "if ((" << ct << ")r" << in.a << " < (" << ct << ")" << in.lo << "LL || ("
+            << ct << ")r" << in.a << " >= (" << ct << ")" << in.hi << "LL) PM_FAIL(" << in.site
+            << ");\n";
+          break;
+        }
+        case PM_OP_FAIL: o << "PM_FAIL(" << in.site << ");\n"; break;
+        case PM_OP_IF: o << "if (r" << in.a << " != 0) {\n"; ++ind; break;
+        case PM_OP_ELSE: o << "} else {\n"; ++ind; break;
+        case PM_OP_ENDIF: o << "}\n"; break;
+        case PM_OP_RET: o << "return (int)r" << in.a << ";\n"; break;
+      }
+    }
+  }
+
+  // Width (0/1) of the implicit row-major index and coordinate types.
+  bool implicit_wide() const {
+    unsigned long long total = 1;
+    for (int i = 0; i < p->n_coords; ++i) {
+      unsigned long long e = (unsigned long long)std::max<long long>(p->extents[i], 1);
+      if (e > 0 && total > ULLONG_MAX / e) return true;
+      total *= e;
+    }
+    return total > 0xFFFFFFFFull;
+  }
+
+  std::string emit() {
+    const int k = p->n_coords;
+    const bool impl = p->implicit != 0;
+    o << "// generated by libmapple_b200 (K1 point program)\n" << kPrelude;
+    o << "__device__ __forceinline__ int pm_point(";
+    for (int i = 0; i < k; ++i) o << "long long c" << i << ", ";
+    o << "int* __restrict__ site_out) {\n";
+    if (max_w == 2 || p->n_regs > 0) {
+      for (int r = 0; r < p->n_regs; ++r)
+        o << "  " << kSigned[w(r)] << " r" << r << " = 0;\n";
+    }
+    body();
+    o << "  PM_FAIL(0xFFFF);\n}\n\n";
+
+    const bool wide = impl && implicit_wide();
+    const char* it = wide ? "unsigned long long" : "unsigned";
+    o << "__device__ __forceinline__ int pm_eval(long long lin, const int* __restrict__ pv, "
+         "int* site) {\n";
+    if (impl) {
+      o << "  " << it << " t = (" << it << ")lin;\n";
+      for (int i = k - 1; i >= 0; --i) {
+        if (i == 0) {
+          o << "  long long c0 = (long long)t;\n";
+        } else {
+          o << "  long long c" << i << " = (long long)(t % (" << it << ")" << p->extents[i]
+            << "ULL); t /= (" << it << ")" << p->extents[i] << "ULL;\n";
+        }
+      }
+      o << "  (void)pv;\n";
+    } else {
+      for (int i = 0; i < k; ++i) o << "  long long c" << i << " = pv[" << i << "];\n";
+      o << "  (void)lin;\n";
+    }
+    o << "  return pm_point(";
+    for (int i = 0; i < k; ++i) o << "c" << i << ", ";
+    o << "site);\n}\n\n";
+
+    const int K = impl ? 0 : k;
+    o << "#define PM_K " << K << "\n";
+    o << R"CUDA(
+__device__ __forceinline__ void pm_report(unsigned long long* status, long long idx, int site) {
+  atomicMin(status, ((unsigned long long)idx << 16) | (unsigned long long)(site & 0xFFFF));
+}
+
+extern "C" __global__ void __launch_bounds__(256)
+pm_map_points(const int* __restrict__ pts, long long n, long long first,
+              int* __restrict__ out, unsigned long long* __restrict__ status, int vec_ok) {
+  const long long ngroups = (n + 3) >> 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += stride) {
+    const long long i0 = g << 2;
+    long long bad_idx = -1;
+    int bad_site = 0;
+    if (vec_ok && i0 + 4 <= n) {
+#if PM_K > 0
+      int buf[4 * PM_K];
+      const int4* src = reinterpret_cast<const int4*>(pts + i0 * PM_K);
+#pragma unroll
+      for (int j = 0; j < PM_K; ++j) {
+        int4 v;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src + j));
+        buf[4 * j] = v.x; buf[4 * j + 1] = v.y; buf[4 * j + 2] = v.z; buf[4 * j + 3] = v.w;
+      }
+#else
+      const int* buf = nullptr;
+#endif
+      int res[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        int site = 0;
+        const int r = pm_eval(first + i0 + v, buf + v * PM_K, &site);
+        if (r < 0 && bad_idx < 0) { bad_idx = i0 + v; bad_site = site; }
+        res[v] = r;
+      }
+      asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};"
+                   :: "l"(out + i0), "r"(res[0]), "r"(res[1]), "r"(res[2]), "r"(res[3]) : "memory");
+    } else {
+      for (int v = 0; v < 4; ++v) {
+        const long long i = i0 + v;
+        if (i >= n) break;
+        int site = 0;
+        const int r = pm_eval(first + i, pts + i * PM_K, &site);
+        if (r < 0 && bad_idx < 0) { bad_idx = i; bad_site = site; }
+        out[i] = r;
+      }
+    }
+    if (bad_idx >= 0) pm_report(status, first + bad_idx, bad_site);
+  }
+}
+)CUDA";
+    return o.str();
+  }
+};
+
+std::mutex g_cache_mu;
+std::unordered_map<std::string, std::vector<char>> g_cubins;
+
+int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cubins.find(src);
+    if (it != g_cubins.end()) {
+      *cubin = it->second;
+      return PM_OK;
+    }
+  }
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "pm_point_program.cu", 0, nullptr, nullptr) !=
+      NVRTC_SUCCESS)
+    return set_error("nvrtcCreateProgram failed"), PM_ERR_NVRTC;
+  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-device-int128", "-lineinfo",
+                        "-default-device", "-w"};
+  nvrtcResult rc = nvrtcCompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    set_error("NVRTC compile failed: %s\n%.4000s", nvrtcGetErrorString(rc), log.c_str());
+    return PM_ERR_NVRTC;
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  cubin->resize(n);
+  nvrtcGetCUBIN(prog, cubin->data());
+  nvrtcDestroyProgram(&prog);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cubins.emplace(src, *cubin);
+  return PM_OK;
+}
+
+int generate(const pm_program* prog, std::string* out) {
+  if (!prog || (prog->n_insns > 0 && !prog->insns) || (prog->n_regs > 0 && !prog->reg_width))
+    return set_error("null program"), PM_ERR_INVALID;
+  if (prog->implicit && prog->n_coords > 0 && !prog->extents)
+    return set_error("implicit program without extents"), PM_ERR_INVALID;
+  Gen g;
+  g.p = prog;
+  int rc = g.check();
+  if (rc) return rc;
+  *out = g.emit();
+  return PM_OK;
+}
+
+}  // namespace
+
+}  // namespace pm
+
+struct pm_plan {
+  CUmodule mod = nullptr;
+  CUfunction fn = nullptr;
+  int n_coords = 0;
+  int implicit = 0;
+  int device = 0;
+};
+
+extern "C" {
+
+int pm_codegen(const pm_program* prog, char* buf, size_t cap, size_t* len) {
+  std::string src;
+  int rc = pm::generate(prog, &src);
+  if (rc) return rc;
+  if (len) *len = src.size();
+  if (buf && cap) {
+    size_t n = std::min(cap - 1, src.size());
+    std::memcpy(buf, src.data(), n);
+    buf[n] = '\0';
+  }
+  return PM_OK;
+}
+
+int pm_compile_check(const pm_program* prog) {
+  std::string src;
+  int rc = pm::generate(prog, &src);
+  if (rc) return rc;
+  std::vector<char> cubin;
+  return pm::nvrtc_compile(src, &cubin);
+}
+
+int pm_plan_create(const pm_program* prog, pm_plan** out) {
+  if (!out) return pm::set_error("null out"), PM_ERR_INVALID;
+  *out = nullptr;
+  std::string src;
+  int rc = pm::generate(prog, &src);
+  if (rc) return rc;
+  std::vector<char> cubin;
+  rc = pm::nvrtc_compile(src, &cubin);
+  if (rc) return rc;
+  const pm::Driver* d = pm::driver();
+  if (!d) return PM_ERR_CUDA;
+  PM_CUDA_TRY(cudaFree(nullptr));  // make sure the primary context exists
+  pm_plan* p = new pm_plan();
+  PM_CUDA_TRY(cudaGetDevice(&p->device));
+  CUresult r = d->moduleLoadData(&p->mod, cubin.data());
+  if (r != CUDA_SUCCESS) {
+    delete p;
+    pm::set_error("cuModuleLoadData failed: CUresult %d", (int)r);
+    return PM_ERR_CUDA;
+  }
+  r = d->moduleGetFunction(&p->fn, p->mod, "pm_map_points");
+  if (r != CUDA_SUCCESS) {
+    d->moduleUnload(p->mod);
+    delete p;
+    pm::set_error("cuModuleGetFunction failed: CUresult %d", (int)r);
+    return PM_ERR_CUDA;
+  }
+  p->n_coords = prog->n_coords;
+  p->implicit = prog->implicit;
+  *out = p;
+  return PM_OK;
+}
+
+void pm_plan_destroy(pm_plan* plan) {
+  if (!plan) return;
+  const pm::Driver* d = pm::driver();
+  if (d && plan->mod) d->moduleUnload(plan->mod);
+  delete plan;
+}
+
+int pm_map_batch(const pm_plan* plan, const int32_t* points, int64_t n, int64_t first,
+                 int32_t* out_proc, uint64_t* status, void* stream) {
+  if (!plan || !out_proc || !status || n < 0 || first < 0)
+    return pm::set_error("pm_map_batch: bad arguments"), PM_ERR_INVALID;
+  if (!plan->implicit && plan->n_coords > 0 && !points)
+    return pm::set_error("pm_map_batch: explicit plan needs points"), PM_ERR_INVALID;
+  if (first + n >= (1LL << 47)) return pm::set_error("pm_map_batch: index too large"), PM_ERR_UNSUPPORTED;
+  if (n == 0) return PM_OK;
+  const pm::Driver* d = pm::driver();
+  if (!d) return PM_ERR_CUDA;
+  const int threads = 256;
+  const long long groups = (n + 3) / 4;
+  long long blocks = (groups + threads - 1) / threads;
+  const long long cap = (long long)pm::num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  int vec_ok = ((uintptr_t)out_proc % 16 == 0) &&
+               (plan->implicit || plan->n_coords == 0 || (uintptr_t)points % 16 == 0);
+  const int32_t* pts = points;
+  long long nn = n, ff = first;
+  void* args[] = {(void*)&pts, (void*)&nn, (void*)&ff, (void*)&out_proc, (void*)&status,
+                  (void*)&vec_ok};
+  PM_CU_TRY(d->launchKernel(plan->fn, (unsigned)blocks, 1, 1, threads, 1, 1, 0,
+                            (CUstream)stream, args, nullptr));
+  return PM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// K2 -- stable ownership partition of mapped points.
+//
+// Reference semantics: expand_shards / shard_policy (tasksim/sim.py:67-120)
+// split an index launch into one leaf per distinct processor, each leaf
+// keeping its points in launch order; proc_counts (cli.py:154-164) counts
+// them.  On the GPU that is a stable counting sort of point indices by
+// processor id (stable_partition.cuh).  Traffic: the 4 B/pt processor id is
+// read by the histogram and by the scatter, the 4 B/pt index written once.
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pm_common.h"
+#include "stable_partition.cuh"
+
+namespace pm {
+namespace {
+
+struct ProcKey {
+  const int* __restrict__ proc;
+  int nbins;
+  unsigned long long* bad;
+  __device__ __forceinline__ int operator()(long long i) const {
+    const int b = __ldg(proc + i);
+    if (b < 0 || b >= nbins) {
+      atomicMin(bad, (unsigned long long)i);
+      return -1;
+    }
+    return b;
+  }
+};
+
+struct PermSink {
+  int* __restrict__ perm;
+  __device__ __forceinline__ void put(long long pos, long long i) const { perm[pos] = (int)i; }
+};
+
+// `bad` is an unsigned atomicMin target that starts at UINT64_MAX; report
+// "no bad id" as -1 (same bit pattern) -- nothing to do.
+}  // namespace
+}  // namespace pm
+
+extern "C" {
+
+size_t pm_partition_scratch_bytes(int64_t n, int32_t nbins) {
+  return pm::part_scratch_bytes(n, nbins);
+}
+
+int pm_partition(const int32_t* proc, int64_t n, int32_t nbins, int64_t* counts,
+                 int64_t* offsets, int32_t* perm, int64_t* bad, void* scratch,
+                 size_t scratch_bytes, void* stream) {
+  if (n < 0 || !counts || !offsets || !bad || (n > 0 && !proc))
+    return pm::set_error("pm_partition: bad arguments"), PM_ERR_INVALID;
+  if (n >= (1LL << 31))
+    return pm::set_error("pm_partition: int32 permutation needs n < 2^31"), PM_ERR_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  PM_CUDA_TRY(cudaMemsetAsync(bad, 0xFF, sizeof(int64_t), s));
+  pm::ProcKey key{proc, nbins, reinterpret_cast<unsigned long long*>(bad)};
+  pm::PermSink sink{perm};
+  return pm::stable_partition(key, sink, perm != nullptr, n, nbins,
+                              reinterpret_cast<long long*>(counts),
+                              reinterpret_cast<long long*>(offsets), scratch, scratch_bytes, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+// Generic stable counting partition used by K2 (points by processor) and K3
+// (halo transfer entries by (src, dst) pair).
+//
+// Items are indexed 0..n-1; `Key::operator()(i)` returns the bin of item i or
+// -1 (no output).  `Sink::put(pos, i)` writes item i at output position pos.
+//
+//   k_part_hist     one CTA per tile: warp-aggregated (match.any) shared
+//                   atomics; hist written bin-major hist[b * ntiles + t]
+//   exclusive scan  of hist -> first output slot of every (bin, tile)
+//   k_part_scatter  per tile, 256 items per round; lanes grouped by bin with
+//                   match.any, rank = popc(peers below), per-warp counts
+//                   (round-tagged) in shared memory give the prefix across
+//                   warps; a running per-bin count carries across rounds.
+//                   Output order inside a bin = item order (stable).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "pm_common.h"
+#include "scan.cuh"
+
+namespace pm {
+namespace {
+
+constexpr int kPartThreads = 256;
+constexpr int kPartWarps = kPartThreads / 32;
+
+inline int part_tile(int nbins) {
+  int m = (nbins + 255) / 256;
+  return 2048 * (m < 1 ? 1 : m);
+}
+
+inline size_t part_scratch_bytes(long long n, int nbins) {
+  if (n <= 0 || nbins <= 0) return 256;
+  const long long tile = part_tile(nbins);
+  const long long ntiles = (n + tile - 1) / tile;
+  const long long len = ntiles * nbins;
+  return (size_t)(len * 8) + scan_scratch_bytes(len) + 256;
+}
+
+template <class Key>
+__global__ void __launch_bounds__(kPartThreads)
+k_part_hist(Key key, long long n, int nbins, int tile, long long ntiles,
+            long long* __restrict__ hist) {
+  extern __shared__ int h[];
+  for (int b = threadIdx.x; b < nbins; b += kPartThreads) h[b] = 0;
+  __syncthreads();
+  const long long start = (long long)blockIdx.x * tile;
+  const int lane = threadIdx.x & 31;
+  for (int off = threadIdx.x; off < tile; off += kPartThreads) {
+    const long long i = start + off;
+    const int b = i < n ? key(i) : -1;
+    if (__any_sync(0xffffffffu, b >= 0)) {
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      if (b >= 0 && lane == __ffs(peers) - 1) atomicAdd(&h[b], __popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += kPartThreads)
+    hist[(long long)b * ntiles + blockIdx.x] = h[b];
+}
+
+template <class Key, class Sink>
+__global__ void __launch_bounds__(kPartThreads)
+k_part_scatter(Key key, Sink sink, long long n, int nbins, int tile, long long ntiles,
+               const long long* __restrict__ pos0) {
+  extern __shared__ int sm[];
+  int* run = sm;         // [nbins]
+  int* wc = sm + nbins;  // [kPartWarps][nbins], (round << 16) | count
+  for (int b = threadIdx.x; b < nbins; b += kPartThreads) run[b] = 0;
+  for (int b = threadIdx.x; b < kPartWarps * nbins; b += kPartThreads) wc[b] = -1;
+  __syncthreads();
+  const long long t = blockIdx.x;
+  const long long start = t * tile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
+  const int rounds = tile / kPartThreads;
+  for (int r = 0; r < rounds; ++r) {
+    const long long i = start + (long long)r * kPartThreads + threadIdx.x;
+    const int b = i < n ? key(i) : -1;
+    const bool any = __any_sync(0xffffffffu, b >= 0);
+    int rank = 0, cnt = 0;
+    if (any) {
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      rank = __popc(peers & below);
+      cnt = __popc(peers);
+      if (b >= 0 && rank == 0) wc[warp * nbins + b] = (r << 16) | cnt;
+    }
+    __syncthreads();
+    if (b >= 0) {
+      int pre = 0;
+      for (int w = 0; w < warp; ++w) {
+        const int v = wc[w * nbins + b];
+        if ((v >> 16) == r) pre += v & 0xFFFF;
+      }
+      sink.put(pos0[(long long)b * ntiles + t] + run[b] + pre + rank, i);
+    }
+    __syncthreads();
+    if (b >= 0 && rank == 0) atomicAdd(&run[b], cnt);
+  }
+}
+
+__global__ void k_part_bin_totals(const long long* __restrict__ scanned, long long ntiles,
+                                  int nbins, const long long* __restrict__ total,
+                                  long long* __restrict__ counts, long long* __restrict__ offsets) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nbins) return;
+  const long long lo = scanned[(long long)b * ntiles];
+  const long long hi = (b + 1 < nbins) ? scanned[(long long)(b + 1) * ntiles] : *total;
+  counts[b] = hi - lo;
+  offsets[b] = lo;
+}
+
+// counts/offsets always; the scatter only when `scatter` is true.
+template <class Key, class Sink>
+int stable_partition(Key key, Sink sink, bool scatter, long long n, int nbins, long long* counts,
+                     long long* offsets, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+  if (nbins <= 0 || nbins > 4096) return set_error("partition: 1..4096 bins"), PM_ERR_INVALID;
+  if (scratch_bytes < part_scratch_bytes(n, nbins))
+    return set_error("partition: scratch too small"), PM_ERR_INVALID;
+  if (n <= 0) {
+    PM_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(long long) * nbins, s));
+    PM_CUDA_TRY(cudaMemsetAsync(offsets, 0, sizeof(long long) * nbins, s));
+    return PM_OK;
+  }
+  const int tile = part_tile(nbins);
+  const long long ntiles = (n + tile - 1) / tile;
+  if (ntiles > 0x7FFFFFFFLL) return set_error("partition: too many tiles"), PM_ERR_UNSUPPORTED;
+  const long long len = ntiles * nbins;
+  long long* hist = reinterpret_cast<long long*>(scratch);
+  void* scan_tmp = reinterpret_cast<char*>(scratch) + len * 8;
+  k_part_hist<Key><<<(unsigned)ntiles, kPartThreads, sizeof(int) * nbins, s>>>(key, n, nbins, tile,
+                                                                             ntiles, hist);
+  PM_CUDA_TRY(cudaGetLastError());
+  int rc = exclusive_scan_i64(hist, len, scan_tmp, s);
+  if (rc) return rc;
+  k_part_bin_totals<<<(nbins + 255) / 256, 256, 0, s>>>(
+      hist, ntiles, nbins, reinterpret_cast<const long long*>(scan_tmp), counts, offsets);
+  PM_CUDA_TRY(cudaGetLastError());
+  if (scatter) {
+    const size_t smem = sizeof(int) * (size_t)nbins * (1 + kPartWarps);
+    if (smem > 48 * 1024)
+      PM_CUDA_TRY(cudaFuncSetAttribute(k_part_scatter<Key, Sink>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_part_scatter<Key, Sink><<<(unsigned)ntiles, kPartThreads, smem, s>>>(key, sink, n, nbins,
+                                                                          tile, ntiles, hist);
+    PM_CUDA_TRY(cudaGetLastError());
+  }
+  return PM_OK;
+}
+
+}  // namespace
+}  // namespace pm

@@ -1,0 +1,81 @@
+"""K3 on the B200: halo transfer lists vs the oracle's per-cell enumeration,
+and totals vs the reference's oracle_boundary_count / surface_volume."""
+
+import itertools
+import random
+
+import pytest
+
+from oracle import mapple_oracle as O
+from paper_2507_17087_b200 import commvol as cv
+from paper_2507_17087_b200.dsl import compile_mapper, parse
+from paper_2507_17087_b200.spaces import MachineShape
+from paper_2507_17087_b200.transfer import halo_lists
+
+pytestmark = pytest.mark.gpu
+
+BLOCK = """
+m = Machine(GPU)
+def block(Tuple p, Tuple s):
+    q = m.merge(0, 1).decompose(0, s)
+    idx = p * q.size / s
+    return q[*idx]
+IndexTaskMap t block
+"""
+
+
+def _entries(tl):
+    out = {}
+    counts = tl.pair_counts.tolist()
+    offs = tl.pair_offsets.tolist()
+    cells = tl.cells.tolist()
+    dims = tl.dims.tolist()
+    for key, c in enumerate(counts):
+        if c:
+            src, dst = divmod(key, tl.nprocs)
+            out[(src, dst)] = list(zip(cells[offs[key]:offs[key] + c], dims[offs[key]:offs[key] + c]))
+    return out
+
+
+def test_random_owners_match_oracle(cuda):
+    torch = cuda
+    rng = random.Random(3)
+    for _ in range(30):
+        rank = rng.choice([1, 2, 3])
+        ext = tuple(rng.randint(1, 9) for _ in range(rank))
+        halo = tuple(rng.randint(0, 3) for _ in range(rank))
+        P = rng.randint(1, 6)
+        cells = list(itertools.product(*map(range, ext)))
+        owner = {c: rng.randrange(P) for c in cells}
+        t = torch.tensor([owner[c] for c in cells], dtype=torch.int32, device="cuda")
+        tl = halo_lists(t, ext, halo, P)
+        assert _entries(tl) == O.halo_entries(owner.__getitem__, ext, halo)
+
+
+@pytest.mark.parametrize("ext,machine,halo", [((12, 18), (1, 6), (1, 1)), ((18, 12), (1, 6), (1, 1)),
+                                              ((37, 23), (2, 3), (2, 1)), ((16, 64), (1, 8), (1, 1)),
+                                              ((9, 10, 11), (2, 4), (1, 2, 1))])
+def test_block_partition_totals_match_reference_models(cuda, ext, machine, halo):
+    fn = compile_mapper(parse(BLOCK), "t", MachineShape("GPU", *machine))
+    ids = fn.map_ispace(ext)
+    tl = halo_lists(ids, ext, halo, machine[0] * machine[1])
+    from paper_2507_17087_b200.factorize import search_optimal
+
+    grid, _ = search_optimal(machine[0] * machine[1], ext)
+    g = cv.BlockGrid(ext, grid)
+    assert tl.total == cv.oracle_boundary_count(g, halo, cap=1 << 40)
+    if all(h == 1 for h in halo):
+        assert tl.total == cv.surface_volume(g)
+    # per pair: every send list has a mirror receive of the same size (block grids)
+    counts = tl.pair_counts.view(tl.nprocs, tl.nprocs)
+    assert (counts == counts.T).all()
+
+
+def test_stencil_32768_counts(cuda):
+    """Config 5: 32768^2 on 8 GPUs, decompose grid (2,4): 262,144 halo cells (h=1)."""
+    fn = compile_mapper(parse(BLOCK), "t", MachineShape("GPU", 1, 8))
+    ext = (32768, 32768)
+    ids = fn.map_ispace(ext)
+    tl = halo_lists(ids, ext, (1, 1), 8, counts_only=True)
+    g = cv.BlockGrid(ext, (2, 4))
+    assert tl.total == cv.oracle_boundary_count(g, (1, 1), cap=1 << 40) == 262144

@@ -1,0 +1,84 @@
+"""The C-ABI library loads, exports every symbol of include/mapple_b200.h, and
+its code generator + NVRTC produce sm_100a cubins (no GPU needed)."""
+
+import re
+from pathlib import Path
+
+import pytest
+
+from conftest import ROOT, mapping_cases
+from paper_2507_17087_b200 import native
+from paper_2507_17087_b200.dsl import compile_mapper, parse
+from paper_2507_17087_b200.spaces import MachineShape
+
+HEADER = ROOT / "include" / "mapple_b200.h"
+
+
+def _declared():
+    text = HEADER.read_text()
+    decl = r"^(?:int|void|size_t|const char\s*\*)\s+(pm_[a-z0-9_]+)\s*\("
+    return sorted(set(re.findall(decl, text, flags=re.M)))
+
+
+def test_every_declared_symbol_is_exported():
+    lib = native.lib()
+    declared = _declared()
+    assert declared, "no pm_* declarations found"
+    for name in declared:
+        assert hasattr(lib, name), name
+        assert name in native.SIGNATURES, f"{name} has no ctypes signature"
+    assert lib.pm_abi_version() == native.ABI_VERSION
+
+
+def test_opcodes_match_header():
+    from paper_2507_17087_b200.dsl import lower as L
+
+    text = HEADER.read_text()
+    for i, name in enumerate(L.OP_NAMES):
+        m = re.search(rf"PM_OP_{name}\s*=\s*(\d+)", text)
+        assert m and int(m.group(1)) == i, name
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "-lelf", str(native.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("case", [c for c in mapping_cases()[:: 37] if isinstance(c["table"], list)])
+def test_codegen_compiles_with_nvrtc(case):
+    prog = parse(case["source"])
+    fn = compile_mapper(prog, case["task"], MachineShape("GPU", *case["machine"]))
+    for implicit in (True, False):
+        pp = fn.program_for(case["ispace"], implicit=implicit, k=len(case["ispace"]))
+        src = pp.source()
+        assert "pm_map_points" in src
+        pp.compile_check()
+
+
+def test_bad_program_is_rejected():
+    import ctypes
+
+    bad = native.PmInsn(99, 0, 0, 0, 0, -1, 0, 0)
+    insns = (native.PmInsn * 1)(bad)
+    widths = (ctypes.c_uint8 * 1)(0)
+    ext = (ctypes.c_int64 * 1)(1)
+    prog = native.PmProgram(1, insns, 1, widths, 1, 1, ext)
+    rc = native.lib().pm_compile_check(ctypes.byref(prog))
+    assert rc == 1
+    assert b"opcode" in native.lib().pm_last_error()
+
+
+def test_device_entry_points_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    fn = compile_mapper(parse(Path(ROOT / "tests" / "golden" / "make_golden.py").read_text()
+                              [:0] + "m = Machine(GPU)\ndef f(Tuple p, Tuple s):\n"
+                              "    return m[0, 0]\nIndexTaskMap t f\n"), "t",
+                        MachineShape("GPU", 1, 1))
+    with pytest.raises(native.NativeError):
+        fn.map_ispace((4,))
