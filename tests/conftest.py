@@ -37,7 +37,7 @@ def cuda_ok() -> bool:
         return False
 
 
-@pytest.fixture
+@pytest.fixture(scope="session")
 def cuda():
     if not cuda_ok():
         pytest.fail("this test needs a GPU (mark: gpu)")
