@@ -1,0 +1,480 @@
+#!/usr/bin/env python
+"""Benchmark: mapped-GEMM TFLOP/s on 1/2/4/8 B200 (decompose vs heuristic) + comm bytes.
+
+Workload (BASELINE.json configs[1]): SUMMA, bf16 inputs, fp32 accumulation,
+M = N = K = 32768, C distributed over the GPUs by a Mapple block mapper
+(`decompose` mapping = headline `value`; the Algorithm-1 heuristic mapping is
+measured in the same run).  Synthetic operands (seeded), 2 GiB each, far
+larger than L2, so no flush is needed between steps.  One step = one full
+multiply: NVLink peer pulls of the SUMMA panels on the copy engines + the
+tcgen05 GEMMs.  Time = CUDA events on the compute stream, max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the reference-side CPU path (the oracle port: numpy
+float64 GEMM on a bounded sample of the same product, all host threads) on
+rank 0 and prints the same JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "mapped-GEMM TFLOP/s at 1/2/4/8 B200 (decompose vs heuristic); comm bytes"
+WORKLOAD = "SUMMA bf16 M=N=K=32768, Mapple block mapping (BASELINE configs[1])"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["bf16_tflops"], d["bf16_tflops_sustained"], d["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+            self.t.join(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -- distributed plumbing -----------------------------------------------------------
+
+
+def init_dist(n_gpus: int):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}; launch with torchrun for N>1")
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+# -- our implementation -----------------------------------------------------------------
+
+
+def run_mapping(args, rank, world, local, mapping, timed=True):
+    import torch
+
+    from paper_2507_17087_b200.executors.summa import MappedGemm
+
+    S = args.size
+    ex = MappedGemm(S, S, S, mapping=mapping, rank=rank, world=world, a_chunks=args.chunks,
+                    seed=1234)
+    cs = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        ex.step()
+    torch.cuda.synchronize()
+    barrier(world)
+    # GEMM launch durations (roofline) are taken from a separate instrumented
+    # pass so the timed loop carries no extra events
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        torch.cuda.synchronize()
+        barrier(world)
+        t0.record(cs)
+        for _ in range(args.steps):
+            ex.step()
+        t1.record(cs)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = t0.elapsed_time(t1) / args.steps
+    ms_max = max_over_ranks(ms, world)
+    # instrumented pass: per-launch GEMM durations on the compute stream
+    launch_ms = []
+    for _ in range(max(2, min(args.steps, 5))):
+        evs = []
+        orig = ex.step
+
+        from paper_2507_17087_b200 import gemm as G
+
+        real = G.tile_gemm
+
+        def timed_gemm(*a, **k):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+            out = real(*a, **k)
+            e1.record(cs)
+            evs.append((e0, e1))
+            return out
+
+        G.tile_gemm = timed_gemm
+        try:
+            orig()
+        finally:
+            G.tile_gemm = real
+        torch.cuda.synchronize()
+        launch_ms += [a.elapsed_time(b) for a, b in evs]
+    res = {
+        "grid": list(ex.layout.grid),
+        "ms_per_step": ms_max,
+        "tflops": 2 * S ** 3 / (ms_max * 1e-3) / 1e12,
+        "comm_bytes_per_gpu_max": int(max_over_ranks(ex.recv_bytes, world)),
+        "comm_bytes_total": int(sum_over_ranks(ex.recv_bytes, world)),
+        "gemm_launch_ms_avg": statistics.mean(launch_ms),
+        "gemm_flops_per_launch": ex.flops / max(1, ex.gemm_launches),
+        "gemm_launches_per_step": ex.gemm_launches,
+        "clocks": sampler.summary(),
+    }
+    return ex, res
+
+
+def run_e2e(args, ex, rank, world):
+    """Same multiply through the public API with host buffers: H2D of this GPU's
+    operand slices from pinned memory, the mapped multiply, D2H of its C block."""
+    import torch
+
+    lay = ex.layout
+    ka, kb = lay.a_slice[rank], lay.b_slice[rank]
+    hA = ex.A[:, ka[0]:ka[1]].contiguous().cpu().pin_memory()
+    hB = ex.Bt[:, kb[0]:kb[1]].contiguous().cpu().pin_memory()
+    hC = torch.empty(ex.C.shape, dtype=ex.C.dtype).pin_memory()
+    cs = torch.cuda.current_stream()
+
+    def step():
+        ex.A[:, ka[0]:ka[1]].copy_(hA, non_blocking=True)
+        ex.Bt[:, kb[0]:kb[1]].copy_(hB, non_blocking=True)
+        if world > 1:  # peers may pull these slices only once they have landed
+            torch.cuda.synchronize()
+            barrier(world)
+        ex.step()
+        hC.copy_(ex.C, non_blocking=True)
+
+    for _ in range(1):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    n = max(1, min(args.steps, 3))
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(cs)
+    for _ in range(n):
+        step()
+    t1.record(cs)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(t0.elapsed_time(t1) / n, world)
+    h2d = sum_over_ranks(hA.numel() * 2 + hB.numel() * 2, world)
+    d2h = sum_over_ranks(hC.numel() * hC.element_size(), world)
+    S = args.size
+    return {"value": 2 * S ** 3 / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+
+def cpu_sample(args, threads=None):
+    """The oracle port on the host: numpy float64 C[0:r, 0:c] of the same product."""
+    import numpy as np
+    import torch
+
+    from oracle.numerics import sample_rows_cols
+    from paper_2507_17087_b200.executors.summa import synth
+
+    S = args.size
+    r, c = args.cpu_rows, args.cpu_cols
+    dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+    A = synth((0, r), (0, S), S, 1234, dev).float().cpu().numpy().astype(np.float64)
+    Bt = synth((0, c), (0, S), S, 1235, dev).float().cpu().numpy().astype(np.float64)
+    t = time.perf_counter()
+    C = sample_rows_cols(A, Bt)
+    dt = time.perf_counter() - t
+    return C, dt, 2.0 * r * c * S
+
+
+def hot_path_kernels(args):
+    """K1 / K2 throughput on config 5 (32768^2 stencil launch, 8-way block mapping)."""
+    import torch
+
+    from paper_2507_17087_b200.dsl import compile_mapper, parse
+    from paper_2507_17087_b200.ownership import partition
+    from paper_2507_17087_b200.spaces import MachineShape
+
+    src = ("m = Machine(GPU)\ndef blk(Tuple p, Tuple s):\n"
+           "    q = m.merge(0, 1).decompose(0, s)\n    return q[*(p * q.size / s)]\n"
+           "IndexTaskMap t blk\n")
+    fn = compile_mapper(parse(src), "t", MachineShape("GPU", 1, 8))
+    L = 32768
+    n = L * L
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    st = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        fn.map_ispace((L, L), out=out, status=st, check=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    e0.record()
+    for _ in range(reps):
+        fn.map_ispace((L, L), out=out, status=st, check=False)
+    e1.record()
+    torch.cuda.synchronize()
+    k1_ms = e0.elapsed_time(e1) / reps
+    partition(out, 8)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(5):
+        partition(out, 8, check=False)
+    e1.record()
+    torch.cuda.synchronize()
+    k2_ms = e0.elapsed_time(e1) / 5
+    _, _, hbm, _ = peaks()
+    k1_gbs = 4 * n / (k1_ms * 1e-3) / 1e9
+    k2_gbs = 12 * n / (k2_ms * 1e-3) / 1e9
+    return {"workload": "stencil 32768^2 launch, decompose block mapper, 1x8 GPUs (configs[4])",
+            "k1_map": {"points_per_s": n / (k1_ms * 1e-3), "ms": k1_ms, "bytes_per_point": 4,
+                       "achieved_gbs": k1_gbs, "frac_hbm": k1_gbs / hbm},
+            "k2_partition": {"ms": k2_ms, "bytes_per_point": 12, "achieved_gbs": k2_gbs,
+                             "frac_hbm": k2_gbs / hbm}}
+
+
+def main_ours(args):
+    import torch
+
+    rank, world, local = init_dist(args.gpus)
+    burst, sustained, hbm, peak_src = peaks()
+    ex, dec = run_mapping(args, rank, world, local, "decompose")
+    e2e = run_e2e(args, ex, rank, world) if not args.no_e2e else None
+    ex.close()
+    del ex
+    torch.cuda.empty_cache()
+    heur = None
+    if not args.decompose_only:
+        ex, heur = run_mapping(args, rank, world, local, "heuristic")
+        ex.close()
+        del ex
+        torch.cuda.empty_cache()
+    extra = {}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        C64, dt, fl = cpu_sample(args)
+        cpu = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": len(os.sched_getaffinity(0)),
+               "kind": "port",
+               "sample": f"numpy float64 C[0:{args.cpu_rows}, 0:{args.cpu_cols}] of the "
+                         f"{args.size}^3 product (full K), {dt:.1f} s"}
+        # parity on the same sample: the GPU's C block starts at row/col 0 here
+        from paper_2507_17087_b200.executors.summa import MappedGemm
+
+        exc = MappedGemm(args.size, args.size, args.size, mapping="decompose", seed=1234)
+        exc.step()
+        torch.cuda.synchronize()
+        got = exc.C[:args.cpu_rows, :args.cpu_cols].double().cpu().numpy()
+        err = float(abs(got - C64).max() / abs(C64).max())
+        extra["parity"] = {"sample": "C[0:%d, 0:%d] vs numpy float64" % (args.cpu_rows, args.cpu_cols),
+                           "max_rel_err": err, "tolerance": 1e-2, "ok": err <= 1e-2}
+        exc.close()
+        del exc
+        torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and not args.no_kernels:
+        extra["hot_path_kernels"] = hot_path_kernels(args)
+    if rank != 0:
+        return
+    peak = sustained if dec["ms_per_step"] * args.steps > 1000 else burst
+    achieved = dec["gemm_flops_per_launch"] / (dec["gemm_launch_ms_avg"] * 1e-3) / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "gemm_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+    line = {
+        "metric": METRIC,
+        "value": dec["tflops"],
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": dec["ms_per_step"],
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded U(-1,1) operands generated on device)",
+        "config": {"workload": WORKLOAD, "M": args.size, "N": args.size, "K": args.size,
+                   "mapping": "decompose", "grid": dec["grid"], "accumulate": "fp32",
+                   "l2": "operands 2 GiB each, larger than L2 (no flush needed)",
+                   "parallelism": f"summa{dec['grid'][0]}x{dec['grid'][1]}"},
+        "e2e": None if e2e is None else {k: e2e[k] for k in
+                                         ("value", "unit", "h2d_bytes_per_step",
+                                          "d2h_bytes_per_step")},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak,
+                     "peak_source": f"{peak_src} {'sustained' if peak == sustained else 'burst'} "
+                                    "bf16 (MEASURED_PEAKS.json)",
+                     "frac_of_burst": achieved / burst,
+                     "kernel": "pm::gemm::k_gemm_bf16 (tcgen05 UMMA 128x256, TMA, TMEM)",
+                     "traffic": traffic},
+        "cpu_baseline": cpu,
+        "clocks": dec["clocks"],
+        "gpu_launches": dec["gemm_launches_per_step"] * args.steps,
+        "comm": {"decompose": {"grid": dec["grid"],
+                               "bytes_per_gpu_max": dec["comm_bytes_per_gpu_max"],
+                               "bytes_total": dec["comm_bytes_total"]}},
+        "decompose_vs_heuristic": None,
+    }
+    if heur is not None:
+        line["comm"]["heuristic"] = {"grid": heur["grid"],
+                                     "bytes_per_gpu_max": heur["comm_bytes_per_gpu_max"],
+                                     "bytes_total": heur["comm_bytes_total"]}
+        line["decompose_vs_heuristic"] = {
+            "heuristic_tflops": heur["tflops"], "heuristic_ms_per_step": heur["ms_per_step"],
+            "speedup": dec["tflops"] / heur["tflops"],
+            "comm_ratio": heur["comm_bytes_total"] / max(1, dec["comm_bytes_total"])}
+    line.update(extra)
+    print(json.dumps(line), flush=True)
+
+
+def main_reference(args):
+    """Reference arm: the CPU path (oracle port) on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle.numerics import sample_rows_cols
+
+    S = args.size
+    r, c = args.cpu_rows, args.cpu_cols
+    rng = np.random.default_rng(1234)
+    A = rng.uniform(-1, 1, (r, S))
+    Bt = rng.uniform(-1, 1, (c, S))
+    for _ in range(max(0, min(args.warmup, 1))):
+        sample_rows_cols(A[:64], Bt[:64])
+    times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t = time.perf_counter()
+        sample_rows_cols(A, Bt)
+        times.append(time.perf_counter() - t)
+    dt = statistics.mean(times)
+    v = 2.0 * r * c * S / dt / 1e12
+    cores = len(os.sched_getaffinity(0))
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": len(times),
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "M": S, "N": S, "K": S, "mapping": "decompose"},
+        "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": f"numpy float64 C[0:{r}, 0:{c}] of the {S}^3 product "
+                                   "(full K) per step; the reference has no GEMM (SURVEY F9)"},
+        "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--size", type=int, default=32768)
+    ap.add_argument("--chunks", type=int, default=4)
+    ap.add_argument("--cpu-rows", type=int, default=2048)
+    ap.add_argument("--cpu-cols", type=int, default=8192)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-kernels", action="store_true")
+    ap.add_argument("--decompose-only", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: the contract needs >= 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        main_reference(args)
+    else:
+        main_ours(args)
+
+
+if __name__ == "__main__":
+    main()

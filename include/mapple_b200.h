@@ -148,6 +148,19 @@ int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t ldb, void* 
                  int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t c_bf16,
                  int32_t accumulate, void* stream);
 
+/* NVLink peer memory for the mapped executors (replaces the Legion/Realm
+ * data movement the paper's runs used; the reference
+ * package models it only as element counts, commvol.py:1-17).
+ *   pm_ipc_handle: 64-byte CUDA IPC handle of the allocation holding ptr and
+ *                  ptr's byte offset inside it;
+ *   pm_ipc_open / pm_ipc_close: map / unmap a peer's allocation;
+ *   pm_copy2d_async: pitched copy-engine copy (peer or local), stream-ordered. */
+int pm_ipc_handle(const void* ptr, void* handle_out, int64_t* offset_out);
+int pm_ipc_open(const void* handle, void** base_out);
+int pm_ipc_close(void* base);
+int pm_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                    int64_t height, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

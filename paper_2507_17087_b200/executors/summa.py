@@ -1,0 +1,250 @@
+"""Mapped SUMMA: C = A @ B on the GPUs of one box, distributed by a Mapple
+block mapper (the paper's matmul workloads).
+
+Planning (once per problem, like the reference's per-ispace prefix,
+dsl/interp.py:407-412):
+  1. the C block launch (M/bs x N/bs points) is mapped to GPUs by a Mapple
+     program on the machine (G GPUs, 1 per node) -- the decompose
+     mapper `m.merge(0,1).decompose(0, ispace)` or the Algorithm-1 heuristic
+     `m.merge(0,1).split(0, g0)` -- with the K1 kernel;
+  2. the K2 kernel partitions the launch into per-GPU ownership lists, from
+     which every GPU's C rectangle, its row group and its column group follow;
+  3. A row-panels and B column-panels are distributed SUMMA style: the GPU
+     owning C rectangle (rows R, cols C) holds A[R, K-slice] and B[K-slice, C],
+     the K-slice being its position inside its row (column) group.
+Execution (one step = one full multiply):
+  * every GPU pulls the A slices of its row group and the B slices of its
+    column group straight from the peers' memory over NVLink with the copy
+    engines (no SM cost, no NCCL kernel competing with the GEMM);
+  * B first, then A in row chunks, so the tcgen05 GEMM (K4) of chunk r runs
+    while chunk r+1 is still in flight; C accumulates in TMEM over the full K.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from .. import native
+from ..dsl import compile_mapper, parse
+from ..factorize import greedy_grid, search_optimal
+from ..spaces import MachineShape
+
+TILE_MAPPERS = """
+m = Machine(GPU)
+def tiles_decompose(Tuple ipoint, Tuple ispace):
+    q = m.merge(0, 1).decompose(0, ispace)
+    return q[*(ipoint * q.size / ispace)]
+def tiles_heuristic(Tuple ipoint, Tuple ispace):
+    q = m.merge(0, 1).split(0, {g0})
+    return q[*(ipoint * q.size / ispace)]
+IndexTaskMap gemm_decompose tiles_decompose
+IndexTaskMap gemm_heuristic tiles_heuristic
+"""
+
+
+@dataclass(frozen=True)
+class Rect:
+    r0: int
+    r1: int
+    c0: int
+    c1: int
+
+
+def rectangles(owner_ids, nbi: int, nbj: int, world: int, block_m: int, block_n: int,
+               M: int, N: int) -> list[Rect]:
+    """Per-rank C rectangle (element coordinates) from the block owner table.
+
+    Fails unless every rank owns one full rectangle of blocks (a block
+    mapping); the SUMMA executor needs a 2D grid.
+    """
+    spans = {}
+    for b, r in enumerate(owner_ids):
+        i, j = divmod(b, nbj)
+        s = spans.setdefault(r, [i, i, j, j, 0])
+        s[0], s[1] = min(s[0], i), max(s[1], i)
+        s[2], s[3] = min(s[2], j), max(s[3], j)
+        s[4] += 1
+    out = []
+    for r in range(world):
+        if r not in spans:
+            raise ValueError(f"GPU {r} owns no C blocks")
+        i0, i1, j0, j1, n = spans[r]
+        if n != (i1 - i0 + 1) * (j1 - j0 + 1):
+            raise ValueError(f"GPU {r} does not own a rectangle of C blocks")
+        out.append(Rect(i0 * block_m, min(M, (i1 + 1) * block_m),
+                        j0 * block_n, min(N, (j1 + 1) * block_n)))
+    return out
+
+
+@dataclass(frozen=True)
+class Layout:
+    rects: list
+    row_group: list        # per rank: ranks sharing its rows, sorted by column start
+    col_group: list        # per rank: ranks sharing its columns, sorted by row start
+    a_slice: list          # per rank: (k0, k1) of the A slice it holds
+    b_slice: list          # per rank: (k0, k1) of the B slice it holds
+    grid: tuple            # (rows of GPUs, cols of GPUs)
+
+
+def summa_layout(rects: list, K: int) -> Layout:
+    world = len(rects)
+    row_group, col_group = [], []
+    for me in rects:
+        rg = sorted((q for q in range(world) if (rects[q].r0, rects[q].r1) == (me.r0, me.r1)),
+                    key=lambda q: rects[q].c0)
+        cg = sorted((q for q in range(world) if (rects[q].c0, rects[q].c1) == (me.c0, me.c1)),
+                    key=lambda q: rects[q].r0)
+        row_group.append(rg)
+        col_group.append(cg)
+    for r in range(world):
+        covered = sum(rects[q].c1 - rects[q].c0 for q in row_group[r])
+        width = max(x.c1 for x in rects) - min(x.c0 for x in rects)
+        if covered != width:
+            raise ValueError("row groups do not tile C: not a 2D processor grid")
+    a_slice, b_slice = [], []
+    for r in range(world):
+        pc, a = len(row_group[r]), row_group[r].index(r)
+        pr, b = len(col_group[r]), col_group[r].index(r)
+        a_slice.append((K * a // pc, K * (a + 1) // pc))
+        b_slice.append((K * b // pr, K * (b + 1) // pr))
+    grid = (len(col_group[0]), len(row_group[0]))
+    return Layout(rects, row_group, col_group, a_slice, b_slice, grid)
+
+
+def comm_bytes(layout: Layout, K: int, elem: int = 2) -> list[int]:
+    """Bytes each GPU receives per multiply (A panels of its row group + B of its column group)."""
+    out = []
+    for r, rc in enumerate(layout.rects):
+        a = (rc.r1 - rc.r0) * sum(layout.a_slice[q][1] - layout.a_slice[q][0]
+                                  for q in layout.row_group[r] if q != r)
+        b = (rc.c1 - rc.c0) * sum(layout.b_slice[q][1] - layout.b_slice[q][0]
+                                  for q in layout.col_group[r] if q != r)
+        out.append((a + b) * elem)
+    return out
+
+
+def mapper_grid(world: int, M: int, N: int, mapping: str) -> tuple:
+    if mapping == "decompose":
+        return search_optimal(world, (M, N))[0]
+    if mapping == "heuristic":
+        return greedy_grid(world, 2)
+    raise ValueError(f"unknown mapping {mapping!r}")
+
+
+def tile_mapper(world: int, mapping: str):
+    g0 = greedy_grid(world, 2)[0]
+    prog = parse(TILE_MAPPERS.format(g0=g0))
+    return compile_mapper(prog, f"gemm_{mapping}", MachineShape("GPU", world, 1))
+
+
+def synth(rows: tuple, cols: tuple, ld: int, seed: int, device):
+    """Deterministic U(-1, 1) bf16 block of a virtual [*, ld] matrix.
+
+    Element (i, k) depends only on (i * ld + k, seed), so every rank can
+    materialise exactly its own slice of the global operands.
+    """
+    torch = native.require_cuda()
+    i = torch.arange(rows[0], rows[1], device=device, dtype=torch.int64).view(-1, 1)
+    k = torch.arange(cols[0], cols[1], device=device, dtype=torch.int64).view(1, -1)
+    x = (i * ld + k) % (1 << 31)
+    x = (x * 1103515245 + 12345 + seed * 7919) % (1 << 31)
+    x = x ^ (x >> 13)
+    x = (x * 69069 + 1) % (1 << 31)
+    return ((x.to(torch.float32) / float(1 << 30)) - 1.0).to(torch.bfloat16)
+
+
+class MappedGemm:
+    """One GPU's share of a mapped SUMMA multiply (see module docstring)."""
+
+    def __init__(self, M: int, N: int, K: int, *, mapping: str = "decompose", rank: int = 0,
+                 world: int = 1, group=None, block: int = 128, a_chunks: int = 4,
+                 seed: int = 0, out_dtype=None):
+        torch = native.require_cuda()
+        from ..gemm import tile_gemm  # noqa: F401  (fail early if the library is missing)
+        from ..ownership import partition
+        from ..peer import PeerBuffers
+
+        self.M, self.N, self.K = M, N, K
+        self.rank, self.world, self.mapping = rank, world, mapping
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        nbi, nbj = -(-M // block), -(-N // block)
+        # 1-2: map the C block launch with the Mapple program (K1) and take
+        # the per-GPU ownership lists (K2)
+        self.mapper = tile_mapper(world, mapping)
+        owners = self.mapper.map_ispace((nbi, nbj))
+        own = partition(owners, world)
+        self.block_counts = own.counts.tolist()
+        self.owner_table = owners.tolist()
+        self.layout = summa_layout(
+            rectangles(self.owner_table, nbi, nbj, world, block, block, M, N), K)
+        rc = self.layout.rects[rank]
+        self.rows, self.cols = (rc.r0, rc.r1), (rc.c0, rc.c1)
+        mr, nc = rc.r1 - rc.r0, rc.c1 - rc.c0
+        # 3: operand buffers with full K; this GPU's own slices live in place
+        self.A = torch.empty(mr, K, dtype=torch.bfloat16, device=self.device)
+        self.Bt = torch.empty(nc, K, dtype=torch.bfloat16, device=self.device)
+        self.C = torch.empty(mr, nc, dtype=out_dtype or torch.float32, device=self.device)
+        ka, kb = self.layout.a_slice[rank], self.layout.b_slice[rank]
+        self.A[:, ka[0]:ka[1]] = synth(self.rows, ka, K, seed, self.device)
+        self.Bt[:, kb[0]:kb[1]] = synth(self.cols, kb, K, seed + 1, self.device)
+        self.peers = PeerBuffers({"A": self.A, "Bt": self.Bt}, rank, world, group)
+        pulls_from = sorted(set(self.layout.row_group[rank] + self.layout.col_group[rank]) - {rank})
+        self.streams = {q: torch.cuda.Stream(device=self.device) for q in pulls_from}
+        nbr = -(-mr // block)
+        n = max(1, min(a_chunks, nbr)) if pulls_from else 1
+        self.chunks = [(min(mr, nbr * c // n * block), min(mr, nbr * (c + 1) // n * block))
+                       for c in range(n)]
+        self.chunks = [(a, b) for a, b in self.chunks if b > a]
+        self.a_chunks = len(self.chunks)
+        self.ev_b = {q: torch.cuda.Event() for q in self.streams}
+        self.ev_a = {(q, c): torch.cuda.Event() for q in self.streams for c in range(self.a_chunks)}
+        self.done = torch.cuda.Event()
+        self.done.record()
+        self.recv_bytes = comm_bytes(self.layout, K)[rank]
+        self.flops = 2 * mr * nc * K
+        self.gemm_launches = 0
+
+    # -- one multiply ---------------------------------------------------------------
+
+    def _pull(self, name, q, row0, nrows, k0, k1, stream):
+        from ..peer import copy2d
+
+        esz = 2
+        pitch = self.K * esz
+        src = self.peers.ptrs[name][q] + (row0 * self.K + k0) * esz
+        dst = self.peers.ptrs[name][self.rank] + (row0 * self.K + k0) * esz
+        copy2d(dst, pitch, src, pitch, (k1 - k0) * esz, nrows, stream)
+
+    def step(self, stream=None):
+        torch = native.require_cuda()
+        from ..gemm import tile_gemm
+
+        cs = stream or torch.cuda.current_stream()
+        lay, me = self.layout, self.rank
+        nc = self.cols[1] - self.cols[0]
+        for q, s in self.streams.items():
+            s.wait_event(self.done)
+            if q in lay.col_group[me]:
+                k0, k1 = lay.b_slice[q]
+                self._pull("Bt", q, 0, nc, k0, k1, s)
+            self.ev_b[q].record(s)
+        for c, (r0, r1) in enumerate(self.chunks):
+            for q, s in self.streams.items():
+                if q in lay.row_group[me]:
+                    k0, k1 = lay.a_slice[q]
+                    self._pull("A", q, r0, r1 - r0, k0, k1, s)
+                self.ev_a[(q, c)].record(s)
+        for q in self.streams:
+            cs.wait_event(self.ev_b[q])
+        launches = 0
+        for c, (r0, r1) in enumerate(self.chunks):
+            for q in self.streams:
+                cs.wait_event(self.ev_a[(q, c)])
+            tile_gemm(self.A[r0:r1], self.Bt, self.C[r0:r1], stream=cs)
+            launches += 1
+        self.done.record(cs)
+        self.gemm_launches = launches
+        return self.C
+
+    def close(self):
+        self.peers.close()

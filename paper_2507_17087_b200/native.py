@@ -54,6 +54,10 @@ SIGNATURES = {
                                      _I32, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
     "pm_gemm_bf16": (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _I32,
                                     _I32, _VP]),
+    "pm_ipc_handle": (ctypes.c_int, [_VP, _VP, ctypes.POINTER(_I64)]),
+    "pm_ipc_open": (ctypes.c_int, [_VP, ctypes.POINTER(_VP)]),
+    "pm_ipc_close": (ctypes.c_int, [_VP]),
+    "pm_copy2d_async": (ctypes.c_int, [_VP, _I64, _VP, _I64, _I64, _I64, _VP]),
 }
 
 _lib = None

@@ -1,0 +1,62 @@
+"""Peer pointers over NVLink for the mapped executors.
+
+Each rank exposes some of its device buffers to the other ranks of the box:
+CUDA IPC handles are exchanged once through `torch.distributed`
+(all_gather_object), then every rank can pull slices of a peer's buffer with
+the copy engines (`copy2d`), leaving all SMs to the tensor-core kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import native
+
+
+class PeerBuffers:
+    """name -> [device pointer of that buffer on every rank]."""
+
+    def __init__(self, tensors: dict, rank: int, world: int, group=None):
+        torch = native.require_cuda()
+        import torch.distributed as dist
+
+        self.rank, self.world = rank, world
+        self._opened = []
+        mine = {}
+        for name, t in tensors.items():
+            h = (ctypes.c_char * 64)()
+            off = ctypes.c_int64(0)
+            native.check(native.lib().pm_ipc_handle(t.data_ptr(), h, ctypes.byref(off)),
+                         "pm_ipc_handle")
+            mine[name] = (bytes(h), off.value)
+        gathered = [None] * world
+        if world > 1:
+            dist.all_gather_object(gathered, mine, group=group)
+        else:
+            gathered = [mine]
+        self.ptrs = {name: [0] * world for name in tensors}
+        cache = {}
+        for r in range(world):
+            for name, (h, off) in gathered[r].items():
+                if r == rank:
+                    self.ptrs[name][r] = tensors[name].data_ptr()
+                    continue
+                base = cache.get((r, h))
+                if base is None:
+                    out = ctypes.c_void_p()
+                    native.check(native.lib().pm_ipc_open(h, ctypes.byref(out)), "pm_ipc_open")
+                    base = cache[(r, h)] = out.value
+                    self._opened.append(base)
+                self.ptrs[name][r] = base + off
+        _ = torch
+
+    def close(self):
+        for base in self._opened:
+            native.lib().pm_ipc_close(base)
+        self._opened = []
+
+
+def copy2d(dst: int, dpitch: int, src: int, spitch: int, width: int, height: int, stream) -> None:
+    """Pitched byte copy on the copy engines (peer or local), stream-ordered."""
+    native.check(native.lib().pm_copy2d_async(dst, dpitch, src, spitch, width, height,
+                                              native.stream_ptr(stream)), "pm_copy2d_async")
