@@ -69,7 +69,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(a),
       "r"(parity)
@@ -331,6 +331,269 @@ k_gemm_bf16(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   }
 }
 
+// ---- 2-CTA variant: UMMA 256x256 issued by the pair's leader ------------------
+//
+// A CTA pair (cluster of 2 on one TPC) owns a 256 x 256 output tile.  Each
+// CTA stages its 128 rows of A and its 128 rows of Bt (half of N) per k-block;
+// the leader's single thread issues tcgen05.mma.cta_group::2 (M=256, N=256,
+// K=16), which reads both CTAs' shared memory and accumulates each CTA's 128
+// rows into that CTA's TMEM.  Per SM this halves the operand bytes read from
+// shared memory per MMA (64 B/clk instead of 96), the limit of the 1-CTA
+// kernel (ncu: tensor pipe 76% active).
+namespace two {
+
+constexpr int kStages2 = 6;
+constexpr int A2_BYTES = 128 * BK * 2;  // 16 KB: this CTA's 128 rows of A
+constexpr int B2_BYTES = 128 * BK * 2;  // 16 KB: this CTA's 128 rows of Bt
+constexpr int STAGE2 = A2_BYTES + B2_BYTES;
+constexpr int SMEM2 = kStages2 * STAGE2 + 1024 + 512;
+constexpr int TM = 256, TN = 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
+  return out;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2sm(const CUtensorMap* map, uint32_t bar_cluster,
+                                             void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                     uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void commit2(uint64_t* bar) {
+  // arrive on the barrier at this smem offset in both CTAs of the pair
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+k_gemm_bf16_2sm(const __grid_constant__ CUtensorMap map_a,
+                const __grid_constant__ CUtensorMap map_b, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kStages2 * A2_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages2 * STAGE2);
+  uint64_t* full = bars;                  // leader's are used (count 2)
+  uint64_t* empty = bars + kStages2;      // per CTA, signalled by the leader's commit
+  uint64_t* tfull = bars + 2 * kStages2;  // per CTA, signalled by the leader's commit
+  uint64_t* tempty = bars + 2 * kStages2 + 2;  // leader's are used (count 8)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kStages2 + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
+  const int tiles_m = (p.M + TM - 1) / TM;
+  const int tiles_n = (p.N + TN - 1) / TN;
+  const int ntiles = tiles_m * tiles_n;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages2; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  auto coords = [&](int t, int& tm, int& tn) {
+    const int per_group = kGroupM * tiles_n;
+    const int g = t / per_group;
+    const int first_m = g * kGroupM;
+    const int gm = min(kGroupM, tiles_m - first_m);
+    const int r = t - g * per_group;
+    tm = first_m + r % gm;
+    tn = r / gm;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full0 = mapa_shared(smem_u32(&full[0]), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        int tm, tn;
+        coords(t, tm, tn);
+        const int am = tm * TM + crank * 128;
+        const int bn = tn * TN + crank * 128;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fb = full0 + stage * 8;
+          if (leader) {
+            mbar_expect_tx(&full[stage], 2 * STAGE2);
+          } else {
+            mbar_arrive_cluster(fb);
+          }
+          tma_load_2sm(&map_a, fb, sa + stage * A2_BYTES, kb * BK, am);
+          tma_load_2sm(&map_b, fb, sb + stage * B2_BYTES, kb * BK, bn);
+          if (++stage == kStages2) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = make_idesc(TM, TN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair; t < ntiles; t += npairs, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * TN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sa + stage * A2_BYTES);
+          const uint32_t b0 = smem_u32(sb + stage * B2_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            mma2(d_tmem, smem_desc_sw128(a0 + k * UMMA_K * 2), smem_desc_sw128(b0 + k * UMMA_K * 2),
+                 idesc, (kb | k) != 0);
+          }
+          commit2(&empty[stage]);
+          if (++stage == kStages2) { stage = 0; phase ^= 1; }
+        }
+        commit2(&tfull[acc]);
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    const int ew = warp - kEpiWarp0;
+    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    int it = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++it) {
+      int tm, tn;
+      coords(t, tm, tn);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = tm * TM + crank * 128 + ew * 32 + lane;
+      const bool row_ok = row < p.M;
+#pragma unroll 1
+      for (int ch = 0; ch < TN / 32; ++ch) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * TN + ch * 32, v);
+        const int col0 = tn * TN + ch * 32;
+        if (!row_ok || col0 >= p.N) continue;
+        const bool full_cols = col0 + 32 <= p.N;
+        if (p.c32) {
+          float* dst = p.c32 + (long long)row * p.ldc + col0;
+          if (full_cols && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              float4 o = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                     __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+              if (p.accumulate) {
+                const float4 c = *reinterpret_cast<const float4*>(dst + j);
+                o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+              }
+              *reinterpret_cast<float4*>(dst + j) = o;
+            }
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j) {
+              float o = __uint_as_float(v[j]);
+              if (p.accumulate) o += dst[j];
+              dst[j] = o;
+            }
+          }
+        } else {
+          __nv_bfloat16* dst = p.c16 + (long long)row * p.ldc + col0;
+          if (full_cols && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint32_t w[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                float x0 = __uint_as_float(v[j + 2 * q]), x1 = __uint_as_float(v[j + 2 * q + 1]);
+                if (p.accumulate) {
+                  x0 += __bfloat162float(dst[j + 2 * q]);
+                  x1 += __bfloat162float(dst[j + 2 * q + 1]);
+                }
+                __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+                w[q] = *reinterpret_cast<uint32_t*>(&h);
+              }
+              *reinterpret_cast<uint4*>(dst + j) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j) {
+              float o = __uint_as_float(v[j]);
+              if (p.accumulate) o += __bfloat162float(dst[j]);
+              dst[j] = __float2bfloat16_rn(o);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
+}  // namespace two
+
 int make_map(const Driver* d, CUtensorMap* map, const void* base, long long rows, long long cols,
              long long ld, int box_rows) {
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -365,10 +628,11 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
     return pm::set_error("pm_gemm_bf16: dimension too large"), PM_ERR_UNSUPPORTED;
   const pm::Driver* d = pm::driver();
   if (!d) return PM_ERR_CUDA;
+  const bool pair = M > 128 && !getenv("PM_GEMM_1SM");
   CUtensorMap ma, mb;
   int rc = make_map(d, &ma, A, M, K, lda, BM);
   if (rc) return rc;
-  rc = make_map(d, &mb, Bt, N, K, ldb, BN);
+  rc = make_map(d, &mb, Bt, N, K, ldb, pair ? 128 : BN);
   if (rc) return rc;
   Params p{};
   p.M = (int)M;
@@ -387,7 +651,39 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
   if (dev >= 0 && dev < 64 && !attr_done[dev]) {
     PM_CUDA_TRY(cudaFuncSetAttribute(k_gemm_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      SMEM_BYTES));
+    PM_CUDA_TRY(cudaFuncSetAttribute(two::k_gemm_bf16_2sm,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, two::SMEM2));
     attr_done[dev] = true;
+  }
+  if (pair) {
+    const long long pairs_needed =
+        ((M + two::TM - 1) / two::TM) * ((N + two::TN - 1) / two::TN);
+    // persistent grid = the number of CTA pairs that can be co-resident
+    static int max_pairs[64] = {0};
+    if (dev >= 0 && dev < 64 && !max_pairs[dev]) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = 2;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.gridDim = dim3(2 * (pm::num_sms() / 2));
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = two::SMEM2;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, two::k_gemm_bf16_2sm, &cfg) != cudaSuccess || n <= 0)
+        n = pm::num_sms() / 2;
+      max_pairs[dev] = n;
+      if (getenv("PM_GEMM_DEBUG")) fprintf(stderr, "pm_gemm: %d co-resident CTA pairs\n", n);
+    }
+    long long pairs = (dev >= 0 && dev < 64) ? max_pairs[dev] : pm::num_sms() / 2;
+    if (pairs_needed < pairs) pairs = pairs_needed;
+    two::k_gemm_bf16_2sm<<<(unsigned)(2 * pairs), kThreads, two::SMEM2, (cudaStream_t)stream>>>(
+        ma, mb, p);
+    PM_CUDA_TRY(cudaGetLastError());
+    return PM_OK;
   }
   const long long ntiles = (long long)p.tiles_m * p.tiles_n;
   int grid = pm::num_sms();
