@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "pm_common.h"
 
@@ -36,7 +38,6 @@ constexpr int UMMA_K = 16;
 constexpr int kStages = 4;
 constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
-constexpr int kGroupM = 16;  // tile raster: groups of 16 M-tiles
 constexpr uint32_t kTmemCols = 512;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_BYTES = BN * BK * 2;  // 32 KB
@@ -69,7 +70,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(a),
       "r"(parity)
@@ -148,14 +149,17 @@ struct Params {
   __nv_bfloat16* c16;
   long long ldc;
   int accumulate;
+  int group_m;  // tile raster: group_m M-tiles advance together across N
+  int debug_nostore;  // experiments only (PM_GEMM_NOSTORE): skip the C stores
+  int tma_store;      // epilogue through smem + TMA bulk store (map_c valid)
 };
 
 __device__ __forceinline__ void tile_coords(int t, const Params& p, int& tm, int& tn) {
   // grouped raster: kGroupM M-tiles advance together across N
-  const int per_group = kGroupM * p.tiles_n;
+  const int per_group = p.group_m * p.tiles_n;
   const int g = t / per_group;
-  const int first_m = g * kGroupM;
-  const int gm = min(kGroupM, p.tiles_m - first_m);
+  const int first_m = g * p.group_m;
+  const int gm = min(p.group_m, p.tiles_m - first_m);
   const int r = t - g * per_group;
   tm = first_m + r % gm;
   tn = r / gm;
@@ -449,10 +453,10 @@ k_gemm_bf16_2sm(const __grid_constant__ CUtensorMap map_a,
   const uint32_t tmem_base = *tmem_holder;
 
   auto coords = [&](int t, int& tm, int& tn) {
-    const int per_group = kGroupM * tiles_n;
+    const int per_group = p.group_m * tiles_n;
     const int g = t / per_group;
-    const int first_m = g * kGroupM;
-    const int gm = min(kGroupM, tiles_m - first_m);
+    const int first_m = g * p.group_m;
+    const int gm = min(p.group_m, tiles_m - first_m);
     const int r = t - g * per_group;
     tm = first_m + r % gm;
     tn = r / gm;
@@ -594,6 +598,305 @@ k_gemm_bf16_2sm(const __grid_constant__ CUtensorMap map_a,
 
 }  // namespace two
 
+// ---- wide 2-CTA variant: pair tile 512 x 256, CTA tile 256 x 256 ------------
+//
+// Same pairing as `two`, but every k-step issues two UMMA 256x256 (rows
+// 0..255 and 256..511 of the pair tile) sharing the B half in shared memory,
+// accumulating into the two 256-column halves of TMEM.  Per MAC this reads
+// 25% fewer operand bytes from L2 than the 256x256 pair tile (ncu: the
+// 256x256 kernel moved 2x the L2 bytes of cuBLAS for 16384^3), which is what
+// bounds the clock under the 1 kW power cap.  With all 512 TMEM columns in
+// use the accumulator is not double-buffered; instead 8 epilogue warps drain
+// the two halves in parallel and the MMA of the next tile starts on a half as
+// soon as that half is drained.
+namespace wide {
+
+using namespace two;
+
+constexpr int kStagesW = 4;
+constexpr int AW_BYTES = 256 * BK * 2;  // 32 KB: this CTA's 2 x 128 rows of A
+constexpr int BW_BYTES = 128 * BK * 2;  // 16 KB: this CTA's 128 rows of Bt
+constexpr int STAGEW = AW_BYTES + BW_BYTES;
+constexpr int EPI_BUF = 32 * 32 * 4;    // per epilogue warp: one 32x32 fp32 box
+constexpr int kEpiWarps = 8;
+constexpr int SMEMW = kStagesW * STAGEW + kEpiWarps * EPI_BUF + 1024 + 512;
+constexpr int WM = 512, WN = 256;
+constexpr int kThreadsW = 384;  // warps 0-3 control, 4-7 drain half 0, 8-11 drain half 1
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y,
+                                             bool add) {
+  if (add) {
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];"
+        ::"l"(map), "r"(smem_u32(src)), "r"(x), "r"(y) : "memory");
+  } else {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+                 ::"l"(map), "r"(smem_u32(src)), "r"(x), "r"(y) : "memory");
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// One warp's 32 rows x 32 columns through shared memory and a TMA store.
+// fp32: 128-byte rows, SWIZZLE_128B (16-byte chunk c of row r at c ^ (r & 7));
+// bf16: 64-byte rows, SWIZZLE_64B (chunk c at c ^ ((r >> 1) & 3)).
+__device__ __forceinline__ void store_chunk_tma(const CUtensorMap* map_c, bool f32, bool add,
+                                                uint8_t* buf, int lane, int row0, int col0,
+                                                const uint32_t (&v)[32]) {
+  if (lane == 0) bulk_wait_read0();  // previous store out of this buffer has read it
+  __syncwarp();
+  if (f32) {
+    uint8_t* rowp = buf + lane * 128;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t a = smem_u32(rowp + ((c ^ (lane & 7)) << 4));
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v[4 * c]),
+                   "r"(v[4 * c + 1]), "r"(v[4 * c + 2]), "r"(v[4 * c + 3])
+                   : "memory");
+    }
+  } else {
+    uint8_t* rowp = buf + lane * 64;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[8 * c + 2 * q]),
+                                                 __uint_as_float(v[8 * c + 2 * q + 1]));
+        w[q] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      const uint32_t a = smem_u32(rowp + ((c ^ ((lane >> 1) & 3)) << 4));
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w[0]), "r"(w[1]),
+                   "r"(w[2]), "r"(w[3])
+                   : "memory");
+    }
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) tma_store_2d(map_c, buf, col0, row0, add);
+}
+
+__device__ __forceinline__ void store_chunk(const Params& p, int row, int col0,
+                                            const uint32_t (&v)[32]) {
+  if (row >= p.M || col0 >= p.N || p.debug_nostore) return;
+  const bool full_cols = col0 + 32 <= p.N;
+  if (p.c32) {
+    float* dst = p.c32 + (long long)row * p.ldc + col0;
+    if (full_cols && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 o = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                               __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+        if (p.accumulate) {
+          const float4 c = *reinterpret_cast<const float4*>(dst + j);
+          o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+        }
+        *reinterpret_cast<float4*>(dst + j) = o;
+      }
+    } else {
+      for (int j = 0; j < 32 && col0 + j < p.N; ++j) {
+        float o = __uint_as_float(v[j]);
+        if (p.accumulate) o += dst[j];
+        dst[j] = o;
+      }
+    }
+  } else {
+    __nv_bfloat16* dst = p.c16 + (long long)row * p.ldc + col0;
+    if (full_cols && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float x0 = __uint_as_float(v[j + 2 * q]), x1 = __uint_as_float(v[j + 2 * q + 1]);
+          if (p.accumulate) {
+            x0 += __bfloat162float(dst[j + 2 * q]);
+            x1 += __bfloat162float(dst[j + 2 * q + 1]);
+          }
+          __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+          w[q] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        *reinterpret_cast<uint4*>(dst + j) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    } else {
+      for (int j = 0; j < 32 && col0 + j < p.N; ++j) {
+        float o = __uint_as_float(v[j]);
+        if (p.accumulate) o += __bfloat162float(dst[j]);
+        dst[j] = __float2bfloat16_rn(o);
+      }
+    }
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
+k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
+                 const __grid_constant__ CUtensorMap map_b,
+                 const __grid_constant__ CUtensorMap map_c, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kStagesW * AW_BYTES;
+  uint8_t* epi = smem + kStagesW * STAGEW;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + kEpiWarps * EPI_BUF);
+  uint64_t* full = bars;                    // leader's (count 2)
+  uint64_t* empty = bars + kStagesW;        // per CTA (leader's commit)
+  uint64_t* tfull = bars + 2 * kStagesW;    // per CTA (leader's commit)
+  uint64_t* tempty = bars + 2 * kStagesW + 1;  // [2] leader's, count 8 each
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kStagesW + 3);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
+  const int tiles_m = (p.M + WM - 1) / WM;
+  const int tiles_n = (p.N + WN - 1) / WN;
+  const int ntiles = tiles_m * tiles_n;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStagesW; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], 8);
+    mbar_init(&tempty[1], 8);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  auto coords = [&](int t, int& tm, int& tn) {
+    const int per_group = p.group_m * tiles_n;
+    const int g = t / per_group;
+    const int first_m = g * p.group_m;
+    const int gm = min(p.group_m, tiles_m - first_m);
+    const int r = t - g * per_group;
+    tm = first_m + r % gm;
+    tn = r / gm;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full0 = mapa_shared(smem_u32(&full[0]), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        int tm, tn;
+        coords(t, tm, tn);
+        const int am = tm * WM + crank * 128;
+        const int bn = tn * WN + crank * 128;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fb = full0 + stage * 8;
+          if (leader) {
+            mbar_expect_tx(&full[stage], 2 * STAGEW);
+          } else {
+            mbar_arrive_cluster(fb);
+          }
+          uint8_t* a = sa + stage * AW_BYTES;
+          tma_load_2sm(&map_a, fb, a, kb * BK, am);
+          tma_load_2sm(&map_a, fb, a + AW_BYTES / 2, kb * BK, am + 256);
+          tma_load_2sm(&map_b, fb, sb + stage * BW_BYTES, kb * BK, bn);
+          if (++stage == kStagesW) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = make_idesc(256, WN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair; t < ntiles; t += npairs, ++it) {
+        const uint32_t tphase = it & 1;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sa + stage * AW_BYTES);
+          const uint32_t b0 = smem_u32(sb + stage * BW_BYTES);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (kb == 0) {  // this half of TMEM must be drained by the epilogue
+              mbar_wait(&tempty[h], tphase ^ 1);
+              tc_fence_after();
+            }
+#pragma unroll
+            for (int k = 0; k < BK / UMMA_K; ++k) {
+              mma2(tmem_base + h * WN, smem_desc_sw128(a0 + h * (AW_BYTES / 2) + k * UMMA_K * 2),
+                   smem_desc_sw128(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0);
+            }
+          }
+          commit2(&empty[stage]);
+          if (++stage == kStagesW) { stage = 0; phase ^= 1; }
+        }
+        commit2(&tfull[0]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int h = (warp - 4) >> 2;  // TMEM half drained by this warp
+    const int q = warp & 3;         // TMEM lane quarter this warp may access
+    const uint32_t tempty_h = mapa_shared(smem_u32(&tempty[h]), 0);
+    int it = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++it) {
+      int tm, tn;
+      coords(t, tm, tn);
+      mbar_wait(&tfull[0], it & 1);
+      tc_fence_after();
+      const int row0 = tm * WM + h * 256 + crank * 128 + q * 32;
+      uint8_t* buf = epi + (warp - 4) * EPI_BUF;
+#pragma unroll 1
+      for (int ch = 0; ch < WN / 32; ++ch) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + h * WN + ch * 32, v);
+        if (p.tma_store) {
+          if (!p.debug_nostore)
+            store_chunk_tma(&map_c, p.c32 != nullptr, p.accumulate != 0, buf, lane, row0,
+                            tn * WN + ch * 32, v);
+        } else {
+          store_chunk(p, row0 + lane, tn * WN + ch * 32, v);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_h);
+    }
+    if (lane == 0) bulk_wait0();
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
+}  // namespace wide
+
 int make_map(const Driver* d, CUtensorMap* map, const void* base, long long rows, long long cols,
              long long ld, int box_rows) {
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -628,7 +931,10 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
     return pm::set_error("pm_gemm_bf16: dimension too large"), PM_ERR_UNSUPPORTED;
   const pm::Driver* d = pm::driver();
   if (!d) return PM_ERR_CUDA;
-  const bool pair = M > 128 && !getenv("PM_GEMM_1SM");
+  // kernel choice: 0 = 1-CTA 128x256, 1 = CTA pair 256x256, 2 = CTA pair 512x256
+  int kind = M <= 128 ? 0 : (M >= 1024 && N >= 256) ? 2 : 1;
+  if (const char* k = getenv("PM_GEMM_KERNEL")) kind = atoi(k);
+  const bool pair = kind != 0;
   CUtensorMap ma, mb;
   int rc = make_map(d, &ma, A, M, K, lda, BM);
   if (rc) return rc;
@@ -645,22 +951,28 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
   p.c16 = c_bf16 ? reinterpret_cast<__nv_bfloat16*>(C) : nullptr;
   p.ldc = ldc;
   p.accumulate = accumulate;
+  p.group_m = kind == 2 ? 6 : 8;
+  if (const char* g = getenv("PM_GEMM_GROUP")) p.group_m = atoi(g) > 0 ? atoi(g) : p.group_m;
+  p.debug_nostore = getenv("PM_GEMM_NOSTORE") ? 1 : 0;
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 64 && !attr_done[dev]) {
+  if (dev < 0 || dev >= 64) return pm::set_error("pm_gemm_bf16: device id"), PM_ERR_UNSUPPORTED;
+  if (!attr_done[dev]) {
     PM_CUDA_TRY(cudaFuncSetAttribute(k_gemm_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      SMEM_BYTES));
     PM_CUDA_TRY(cudaFuncSetAttribute(two::k_gemm_bf16_2sm,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, two::SMEM2));
+    PM_CUDA_TRY(cudaFuncSetAttribute(wide::k_gemm_bf16_wide,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, wide::SMEMW));
     attr_done[dev] = true;
   }
   if (pair) {
-    const long long pairs_needed =
-        ((M + two::TM - 1) / two::TM) * ((N + two::TN - 1) / two::TN);
     // persistent grid = the number of CTA pairs that can be co-resident
-    static int max_pairs[64] = {0};
-    if (dev >= 0 && dev < 64 && !max_pairs[dev]) {
+    const bool use_wide = kind == 2;
+    static int max_pairs[64][2] = {{0}};
+    int& mp = max_pairs[dev][use_wide];
+    if (!mp) {
       cudaLaunchConfig_t cfg = {};
       cudaLaunchAttribute attr;
       attr.id = cudaLaunchAttributeClusterDimension;
@@ -668,20 +980,46 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
       attr.val.clusterDim.y = 1;
       attr.val.clusterDim.z = 1;
       cfg.gridDim = dim3(2 * (pm::num_sms() / 2));
-      cfg.blockDim = dim3(kThreads);
-      cfg.dynamicSmemBytes = two::SMEM2;
+      cfg.blockDim = dim3(use_wide ? wide::kThreadsW : kThreads);
+      cfg.dynamicSmemBytes = use_wide ? wide::SMEMW : two::SMEM2;
       cfg.attrs = &attr;
       cfg.numAttrs = 1;
       int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, two::k_gemm_bf16_2sm, &cfg) != cudaSuccess || n <= 0)
-        n = pm::num_sms() / 2;
-      max_pairs[dev] = n;
+      cudaError_t e = use_wide ? cudaOccupancyMaxActiveClusters(&n, wide::k_gemm_bf16_wide, &cfg)
+                               : cudaOccupancyMaxActiveClusters(&n, two::k_gemm_bf16_2sm, &cfg);
+      if (e != cudaSuccess || n <= 0) n = pm::num_sms() / 2;
+      mp = n;
       if (getenv("PM_GEMM_DEBUG")) fprintf(stderr, "pm_gemm: %d co-resident CTA pairs\n", n);
     }
-    long long pairs = (dev >= 0 && dev < 64) ? max_pairs[dev] : pm::num_sms() / 2;
+    const long long tm = use_wide ? wide::WM : two::TM, tn = use_wide ? wide::WN : two::TN;
+    const long long pairs_needed = ((M + tm - 1) / tm) * ((N + tn - 1) / tn);
+    long long pairs = mp;
     if (pairs_needed < pairs) pairs = pairs_needed;
-    two::k_gemm_bf16_2sm<<<(unsigned)(2 * pairs), kThreads, two::SMEM2, (cudaStream_t)stream>>>(
-        ma, mb, p);
+    if (use_wide) {
+      CUtensorMap mc;
+      std::memset(&mc, 0, sizeof(mc));
+      const int esize = c_bf16 ? 2 : 4;
+      p.tma_store = ((ldc * esize) % 16 == 0) && ((uintptr_t)C % 16 == 0) &&
+                    !(accumulate && c_bf16) && !getenv("PM_GEMM_DIRECT_STORE");
+      if (p.tma_store) {
+        cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+        cuuint64_t strides[1] = {(cuuint64_t)(ldc * esize)};
+        cuuint32_t box[2] = {32, 32};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = d->tensorMapEncodeTiled(
+            &mc, c_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C,
+            dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            c_bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+          return pm::set_error("cuTensorMapEncodeTiled(C) failed: %d", (int)r), PM_ERR_CUDA;
+      }
+      wide::k_gemm_bf16_wide<<<(unsigned)(2 * pairs), wide::kThreadsW, wide::SMEMW,
+                               (cudaStream_t)stream>>>(ma, mb, mc, p);
+    } else {
+      two::k_gemm_bf16_2sm<<<(unsigned)(2 * pairs), kThreads, two::SMEM2,
+                             (cudaStream_t)stream>>>(ma, mb, p);
+    }
     PM_CUDA_TRY(cudaGetLastError());
     return PM_OK;
   }

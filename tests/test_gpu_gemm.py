@@ -38,9 +38,9 @@ def test_gemm_matches_fp64(cuda, M, N, K):
     assert _rel(C, R) < 1e-3
 
 
-def test_gemm_accumulate_and_bf16_out(cuda):
+@pytest.mark.parametrize("M,N,K", [(512, 768, 256), (2048, 1280, 512), (1100, 900, 192)])
+def test_gemm_accumulate_and_bf16_out(cuda, M, N, K):
     torch = cuda
-    M, N, K = 512, 768, 256
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     Bt = torch.randn(N, K, device="cuda").to(torch.bfloat16)
     C0 = torch.randn(M, N, device="cuda")
