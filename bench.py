@@ -54,12 +54,14 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.window = None
 
-    def __enter__(self):
+    def start(self):
+        """Start sampling (call before warm-up so samples exist in the timed window)."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -69,10 +71,14 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
-    def __exit__(self, *exc):
+    def mark(self, t0: float, t1: float):
+        self.window = (t0, t1)
+
+    def stop(self):
         if self.proc:
+            time.sleep(0.12)
             self.proc.terminate()
             self.proc.wait(timeout=5)
             self.t.join(timeout=5)
@@ -80,7 +86,11 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.window:
+            inside = [l for l in lines if self.window[0] - 0.06 <= l[0] <= self.window[1] + 0.06]
+            lines = inside or lines[-3:]
+        for _, ln in lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -160,6 +170,7 @@ def run_mapping(args, rank, world, local, mapping, timed=True):
     ex = MappedGemm(S, S, S, mapping=mapping, rank=rank, world=world, a_chunks=args.chunks,
                     seed=1234)
     cs = torch.cuda.current_stream()
+    sampler = ClockSampler(local).start()
     for _ in range(args.warmup):
         ex.step()
     torch.cuda.synchronize()
@@ -167,15 +178,16 @@ def run_mapping(args, rank, world, local, mapping, timed=True):
     # GEMM launch durations (roofline) are taken from a separate instrumented
     # pass so the timed loop carries no extra events
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local)
-    with sampler:
-        torch.cuda.synchronize()
-        barrier(world)
-        t0.record(cs)
-        for _ in range(args.steps):
-            ex.step()
-        t1.record(cs)
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    w0 = time.time()
+    t0.record(cs)
+    for _ in range(args.steps):
+        ex.step()
+    t1.record(cs)
+    torch.cuda.synchronize()
+    sampler.mark(w0, time.time())
+    sampler.stop()
     barrier(world)
     ms = t0.elapsed_time(t1) / args.steps
     ms_max = max_over_ranks(ms, world)
@@ -474,6 +486,11 @@ def main():
         main_reference(args)
     else:
         main_ours(args)
+        if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
 
 
 if __name__ == "__main__":

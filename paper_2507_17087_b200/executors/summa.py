@@ -158,7 +158,7 @@ class MappedGemm:
 
     def __init__(self, M: int, N: int, K: int, *, mapping: str = "decompose", rank: int = 0,
                  world: int = 1, group=None, block: int = 128, a_chunks: int = 4,
-                 seed: int = 0, out_dtype=None):
+                 seed: int = 0, out_dtype=None, copy_streams: int = 4):
         torch = native.require_cuda()
         from ..gemm import tile_gemm  # noqa: F401  (fail early if the library is missing)
         from ..ownership import partition
@@ -188,25 +188,82 @@ class MappedGemm:
         self.A[:, ka[0]:ka[1]] = synth(self.rows, ka, K, seed, self.device)
         self.Bt[:, kb[0]:kb[1]] = synth(self.cols, kb, K, seed + 1, self.device)
         self.peers = PeerBuffers({"A": self.A, "Bt": self.Bt}, rank, world, group)
-        pulls_from = sorted(set(self.layout.row_group[rank] + self.layout.col_group[rank]) - {rank})
-        self.streams = {q: torch.cuda.Stream(device=self.device) for q in pulls_from}
-        nbr = -(-mr // block)
-        n = max(1, min(a_chunks, nbr)) if pulls_from else 1
-        self.chunks = [(min(mr, nbr * c // n * block), min(mr, nbr * (c + 1) // n * block))
-                       for c in range(n)]
-        self.chunks = [(a, b) for a, b in self.chunks if b > a]
-        self.a_chunks = len(self.chunks)
-        self.ev_b = {q: torch.cuda.Event() for q in self.streams}
-        self.ev_a = {(q, c): torch.cuda.Event() for q in self.streams for c in range(self.a_chunks)}
+        self._plan(block, a_chunks, copy_streams)
         self.done = torch.cuda.Event()
         self.done.record()
         self.recv_bytes = comm_bytes(self.layout, K)[rank]
         self.flops = 2 * mr * nc * K
-        self.gemm_launches = 0
+        self.gemm_launches = len(self.gemms)
+
+    # -- schedule (built once) -------------------------------------------------------
+
+    def _plan(self, block, a_chunks, copy_streams):
+        """K panels ordered by how much of them is local, then pulls per panel.
+
+        A panel is a K-range on which both operands each come from a single GPU
+        (mine or a peer of my row / column group).  Panels whose operands are
+        both local are multiplied first -- no waiting -- while the copy engines
+        bring in the others; remote panels are split into row chunks of A so the
+        GEMM of chunk c overlaps the pull of chunk c+1.  The first panel writes
+        C, later panels accumulate into it (TMA reduce-add epilogue).
+        """
+        torch = native.require_cuda()
+        lay, me, K = self.layout, self.rank, self.K
+        mr, nc = self.rows[1] - self.rows[0], self.cols[1] - self.cols[0]
+        cuts = {0, K}
+        for q in lay.row_group[me]:
+            cuts.update(lay.a_slice[q])
+        for q in lay.col_group[me]:
+            cuts.update(lay.b_slice[q])
+        cuts = sorted(cuts)
+        panels = []
+        for k0, k1 in zip(cuts, cuts[1:]):
+            if k1 <= k0:
+                continue
+            a_src = next(q for q in lay.row_group[me] if lay.a_slice[q][0] <= k0 and k1 <= lay.a_slice[q][1])
+            b_src = next(q for q in lay.col_group[me] if lay.b_slice[q][0] <= k0 and k1 <= lay.b_slice[q][1])
+            remote = (a_src != me) * mr * (k1 - k0) + (b_src != me) * nc * (k1 - k0)
+            panels.append((remote, k0, k1, a_src, b_src))
+        panels.sort()
+        nbr = -(-mr // block)
+        n = max(1, min(a_chunks, nbr))
+        chunks = [(min(mr, nbr * c // n * block), min(mr, nbr * (c + 1) // n * block))
+                  for c in range(n)]
+        chunks = [(a, b) for a, b in chunks if b > a]
+        any_remote = any(p[0] for p in panels)
+        self.copy_streams = ([torch.cuda.Stream(device=self.device) for _ in range(copy_streams)]
+                             if any_remote else [])
+        self.pulls = []   # (name, src rank, row0, rows, k0, k1, stream index, event)
+        self.gemms = []   # (r0, r1, k0, k1, accumulate, [events to wait for])
+        first = True
+        rr = 0
+
+        def pull(name, q, row0, rows, k0, k1):
+            nonlocal rr
+            evs = []
+            pieces = min(len(self.copy_streams), max(1, rows // block))
+            for i in range(pieces):
+                a = row0 + rows * i // pieces
+                b = row0 + rows * (i + 1) // pieces
+                ev = torch.cuda.Event()
+                self.pulls.append((name, q, a, b - a, k0, k1, rr % len(self.copy_streams), ev))
+                rr += 1
+                evs.append(ev)
+            return evs
+
+        for _, k0, k1, a_src, b_src in panels:
+            b_evs = pull("Bt", b_src, 0, nc, k0, k1) if b_src != me else []
+            for r0, r1 in (chunks if a_src != me else [(0, mr)]):
+                a_evs = pull("A", a_src, r0, r1 - r0, k0, k1) if a_src != me else []
+                self.gemms.append((r0, r1, k0, k1, not first, b_evs + a_evs))
+                b_evs = []  # later chunks of this panel are ordered after the first
+            first = False
+        self.panels = [(k0, k1, a_src, b_src) for _, k0, k1, a_src, b_src in panels]
+        self.chunks = chunks
 
     # -- one multiply ---------------------------------------------------------------
 
-    def _pull(self, name, q, row0, nrows, k0, k1, stream):
+    def _copy(self, name, q, row0, nrows, k0, k1, stream):
         from ..peer import copy2d
 
         esz = 2
@@ -216,34 +273,23 @@ class MappedGemm:
         copy2d(dst, pitch, src, pitch, (k1 - k0) * esz, nrows, stream)
 
     def step(self, stream=None):
+        """One full multiply, stream-ordered (no host synchronisation)."""
         torch = native.require_cuda()
         from ..gemm import tile_gemm
 
         cs = stream or torch.cuda.current_stream()
-        lay, me = self.layout, self.rank
-        nc = self.cols[1] - self.cols[0]
-        for q, s in self.streams.items():
-            s.wait_event(self.done)
-            if q in lay.col_group[me]:
-                k0, k1 = lay.b_slice[q]
-                self._pull("Bt", q, 0, nc, k0, k1, s)
-            self.ev_b[q].record(s)
-        for c, (r0, r1) in enumerate(self.chunks):
-            for q, s in self.streams.items():
-                if q in lay.row_group[me]:
-                    k0, k1 = lay.a_slice[q]
-                    self._pull("A", q, r0, r1 - r0, k0, k1, s)
-                self.ev_a[(q, c)].record(s)
-        for q in self.streams:
-            cs.wait_event(self.ev_b[q])
-        launches = 0
-        for c, (r0, r1) in enumerate(self.chunks):
-            for q in self.streams:
-                cs.wait_event(self.ev_a[(q, c)])
-            tile_gemm(self.A[r0:r1], self.Bt, self.C[r0:r1], stream=cs)
-            launches += 1
+        for s in self.copy_streams:
+            s.wait_event(self.done)  # the previous multiply no longer reads A / Bt
+        for name, q, row0, rows, k0, k1, si, ev in self.pulls:
+            s = self.copy_streams[si]
+            self._copy(name, q, row0, rows, k0, k1, s)
+            ev.record(s)
+        for r0, r1, k0, k1, acc, evs in self.gemms:
+            for ev in evs:
+                cs.wait_event(ev)
+            tile_gemm(self.A[r0:r1, k0:k1], self.Bt[:, k0:k1], self.C[r0:r1], accumulate=acc,
+                      stream=cs)
         self.done.record(cs)
-        self.gemm_launches = launches
         return self.C
 
     def close(self):
