@@ -230,6 +230,39 @@ def run_mapping(args, rank, world, local, mapping, timed=True):
     return ex, res
 
 
+def run_3d(args, rank, world, local, M, N, K, mapping):
+    """Time one 3-D mapped multiply (Johnson / COSMA grid) with the fused
+    GEMM + NVLink reduce-scatter; max over ranks of CUDA-event time."""
+    import torch
+
+    from paper_2507_17087_b200.executors.grid3d import MappedGemm3D
+
+    ex = MappedGemm3D(M, N, K, mapping=mapping, rank=rank, world=world, seed=99)
+    cs = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        ex.step()
+    ex.result()
+    torch.cuda.synchronize()
+    barrier(world)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(3, args.steps // 2)
+    t0.record(cs)
+    for _ in range(steps):
+        ex.step()
+    ex.result()  # the last step's reduce-adds from the peers have landed
+    t1.record(cs)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(t0.elapsed_time(t1) / steps, world)
+    res = {"grid": list(ex.grid), "ms_per_step": ms,
+           "tflops": 2.0 * M * N * K / (ms * 1e-3) / 1e12,
+           "comm_bytes_per_gpu": ex.comm, "steps": steps,
+           "gpu_launches_per_step": ex.gemm_launches}
+    ex.close()
+    del ex
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_e2e(args, ex, rank, world):
     """Same multiply through the public API with host buffers: H2D of this GPU's
     operand slices from pinned memory, the mapped multiply, D2H of its C block."""
@@ -283,9 +316,14 @@ def cpu_sample(args, threads=None):
     dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
     A = synth((0, r), (0, S), S, 1234, dev).float().cpu().numpy().astype(np.float64)
     Bt = synth((0, c), (0, S), S, 1235, dev).float().cpu().numpy().astype(np.float64)
+    # repeat the bounded sample until ~10 s of host work (contract: 10-30 s)
     t = time.perf_counter()
     C = sample_rows_cols(A, Bt)
-    dt = time.perf_counter() - t
+    reps = 1
+    while time.perf_counter() - t < args.cpu_seconds:
+        sample_rows_cols(A, Bt)
+        reps += 1
+    dt = (time.perf_counter() - t) / reps
     return C, dt, 2.0 * r * c * S
 
 
@@ -351,13 +389,26 @@ def main_ours(args):
         del ex
         torch.cuda.empty_cache()
     extra = {}
+    if not args.no_3d:
+        # BASELINE configs[2] (Johnson 3D, square) and configs[3] (COSMA, rectangular)
+        wl = {}
+        for name, (M, N, K) in (("johnson3d", (args.size,) * 3),
+                                ("cosma", (2 * args.size, args.size // 2, args.size // 2))):
+            d = run_3d(args, rank, world, local, M, N, K, "decompose")
+            h = run_3d(args, rank, world, local, M, N, K, "heuristic")
+            wl[name] = {"M": M, "N": N, "K": K, "decompose": d, "heuristic": h,
+                        "speedup": d["tflops"] / h["tflops"],
+                        "comm_ratio": h["comm_bytes_per_gpu"]["total"] /
+                        max(1, d["comm_bytes_per_gpu"]["total"])}
+        extra["workloads_3d"] = wl
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         C64, dt, fl = cpu_sample(args)
         cpu = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": len(os.sched_getaffinity(0)),
                "kind": "port",
                "sample": f"numpy float64 C[0:{args.cpu_rows}, 0:{args.cpu_cols}] of the "
-                         f"{args.size}^3 product (full K), {dt:.1f} s"}
+                         f"{args.size}^3 product (full K), {dt:.2f} s each, repeated for "
+                         f"~{args.cpu_seconds:.0f} s"}
         # parity on the same sample: the GPU's C block starts at row/col 0 here
         from paper_2507_17087_b200.executors.summa import MappedGemm
 
@@ -445,10 +496,14 @@ def main_reference(args):
     for _ in range(max(0, min(args.warmup, 1))):
         sample_rows_cols(A[:64], Bt[:64])
     times = []
-    for _ in range(max(1, min(args.steps, 3))):
+    nsteps = max(1, min(args.steps, 3))
+    for _ in range(nsteps):  # each step: the bounded sample, repeated for ~cpu_seconds/nsteps
         t = time.perf_counter()
-        sample_rows_cols(A, Bt)
-        times.append(time.perf_counter() - t)
+        reps = 0
+        while reps == 0 or time.perf_counter() - t < args.cpu_seconds / nsteps:
+            sample_rows_cols(A, Bt)
+            reps += 1
+        times.append((time.perf_counter() - t) / reps)
     dt = statistics.mean(times)
     v = 2.0 * r * c * S / dt / 1e12
     cores = len(os.sched_getaffinity(0))
@@ -479,6 +534,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kernels", action="store_true")
     ap.add_argument("--decompose-only", action="store_true")
+    ap.add_argument("--no-3d", action="store_true", help="skip the Johnson / COSMA workloads")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="host seconds spent on the CPU baseline sample")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: the contract needs >= 3 warm-up steps", file=sys.stderr)

@@ -143,7 +143,9 @@ int pm_halo_lists(const int32_t* owner, const int64_t* ext, int32_t rank,
  * accumulation.  A is row-major (K contiguous, lda >= K); B is given
  * transposed as Bt[N,K] row-major (K contiguous, ldb >= K).  C is row-major
  * fp32 (ldc >= N) or bf16 when c_bf16 != 0; accumulate != 0 adds into C.
- * M, N multiples of 128 and K a multiple of 64 (PM_ERR_UNSUPPORTED otherwise). */
+ * accumulate: 0 = overwrite, 1 = C += AB, 2 = C += AB with element-wise atomic
+ * reduce-add (TMA .add; C may be a peer GPU's IPC-mapped buffer, several GPUs may add
+ * concurrently; fp32 only).  lda, ldb % 8 == 0, 16-byte aligned A, Bt. */
 int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t ldb, void* C,
                  int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t c_bf16,
                  int32_t accumulate, void* stream);

@@ -934,6 +934,13 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
   // kernel choice: 0 = 1-CTA 128x256, 1 = CTA pair 256x256, 2 = CTA pair 512x256
   int kind = M <= 128 ? 0 : (M >= 1024 && N >= 256) ? 2 : 1;
   if (const char* k = getenv("PM_GEMM_KERNEL")) kind = atoi(k);
+  // accumulate == 2: element-wise atomic reduce-add (TMA .add), e.g. several
+  // GPUs adding partial products into one C over NVLink
+  const bool atomic_add = accumulate == 2;
+  if (atomic_add) {
+    if (c_bf16) return pm::set_error("pm_gemm_bf16: atomic accumulate needs fp32 C"), PM_ERR_UNSUPPORTED;
+    kind = 2;
+  }
   const bool pair = kind != 0;
   CUtensorMap ma, mb;
   int rc = make_map(d, &ma, A, M, K, lda, BM);
@@ -950,7 +957,7 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
   p.c32 = c_bf16 ? nullptr : reinterpret_cast<float*>(C);
   p.c16 = c_bf16 ? reinterpret_cast<__nv_bfloat16*>(C) : nullptr;
   p.ldc = ldc;
-  p.accumulate = accumulate;
+  p.accumulate = accumulate != 0;
   p.group_m = kind == 2 ? 6 : 8;
   if (const char* g = getenv("PM_GEMM_GROUP")) p.group_m = atoi(g) > 0 ? atoi(g) : p.group_m;
   p.debug_nostore = getenv("PM_GEMM_NOSTORE") ? 1 : 0;
@@ -1001,6 +1008,9 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
       const int esize = c_bf16 ? 2 : 4;
       p.tma_store = ((ldc * esize) % 16 == 0) && ((uintptr_t)C % 16 == 0) &&
                     !(accumulate && c_bf16) && !getenv("PM_GEMM_DIRECT_STORE");
+      if (atomic_add && !p.tma_store)
+        return pm::set_error("pm_gemm_bf16: atomic accumulate needs ldc %% 4 == 0 and a "
+                             "16-byte aligned C"), PM_ERR_UNSUPPORTED;
       if (p.tma_store) {
         cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
         cuuint64_t strides[1] = {(cuuint64_t)(ldc * esize)};

@@ -1,0 +1,191 @@
+"""Mapped 3-D matmul (Johnson 3D, COSMA; BASELINE configs[2] and [3]) with the
+depth reduction fused into the GEMM epilogue over NVLink.
+
+The processor grid (pm, pn, pk) splits M, N and K.  It comes from the
+`decompose` optimizer over the matrix extents (search_optimal(G, (M, N, K)),
+reference factorize.py:166-188) or from the Algorithm-1 heuristic
+(greedy_grid(G, 3), factorize.py:191-206); the grid launch is then mapped
+onto the GPUs by a Mapple program (K1) -- the same role the paper's
+`johnson_mm` / `cosma_mm` mappers play.
+
+GPU (a, b, c) computes the partial product A[a, c] * B[c, b] over K block c:
+  * initial layout (3-D): it holds rows-part b of A[a, c] and cols-part a of
+    B[c, b]; the rest of both blocks is pulled from the peers of its
+    n-group / m-group by the copy engines (all-gather, no SMs);
+  * reduce-scatter over c: C[a, b] rows are split among the pk GPUs of the
+    k-group; the GEMM is launched once per destination row range and its
+    epilogue reduce-adds the tile straight into the owner's C buffer over
+    NVLink (TMA `cp.reduce.async.bulk.tensor .add` on an IPC-mapped pointer) --
+    the collective is fused into the GEMM, there is no separate NCCL call.
+C is double-buffered; one stream-ordered barrier per step (a 4-byte NCCL
+all-reduce) separates the zeroing of a buffer from the peers' adds into it.
+"""
+
+from __future__ import annotations
+
+from math import prod
+
+from .. import native
+from ..dsl import compile_mapper, parse
+from ..factorize import greedy_grid, search_optimal
+from ..spaces import MachineShape
+from .summa import synth
+
+GRID3D_MAPPER = """
+m = Machine(GPU)
+def grid3d(Tuple ipoint, Tuple ispace):
+    q = m.merge(0, 1).decompose(0, ispace)
+    return q[*ipoint]
+IndexTaskMap gemm3d grid3d
+"""
+
+
+def grid_for(world: int, M: int, N: int, K: int, mapping: str) -> tuple:
+    if mapping == "decompose":
+        return tuple(search_optimal(world, (M, N, K))[0])
+    if mapping == "heuristic":
+        return tuple(greedy_grid(world, 3))
+    raise ValueError(mapping)
+
+
+def split(n: int, parts: int, i: int) -> tuple:
+    return (n * i // parts, n * (i + 1) // parts)
+
+
+def comm_bytes_3d(M, N, K, grid) -> dict:
+    """Per-GPU bytes: A/B all-gathers (bf16) and the C reduce-scatter (fp32)."""
+    pm, pn, pk = grid
+    Mb, Nb, Kb = M / pm, N / pn, K / pk
+    a = Mb * Kb * (1 - 1 / pn) * 2
+    b = Kb * Nb * (1 - 1 / pm) * 2
+    c = Mb * Nb * (1 - 1 / pk) * 4
+    return {"a_gather": int(a), "b_gather": int(b), "c_reduce_scatter": int(c),
+            "total": int(a + b + c)}
+
+
+class MappedGemm3D:
+    def __init__(self, M, N, K, *, mapping="decompose", rank=0, world=1, group=None, seed=0,
+                 grid=None, block=256):
+        torch = native.require_cuda()
+        import torch.distributed as dist
+
+        from ..peer import PeerBuffers
+
+        self.M, self.N, self.K = M, N, K
+        self.rank, self.world, self.group = rank, world, group
+        self.grid = tuple(grid) if grid else grid_for(world, M, N, K, mapping)
+        if prod(self.grid) != world:
+            raise ValueError(f"grid {self.grid} does not cover {world} GPUs")
+        pm, pn, pk = self.grid
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        # map the (pm, pn, pk) launch onto the GPUs with the Mapple program (K1)
+        fn = compile_mapper(parse(GRID3D_MAPPER), "gemm3d", MachineShape("GPU", world, 1))
+        owners = fn.map_ispace(self.grid).tolist()
+        if sorted(owners) != list(range(world)):
+            raise ValueError("the grid mapping is not a bijection onto the GPUs")
+        self.owner = {}
+        for lin, r in enumerate(owners):
+            a, rem = divmod(lin, pn * pk)
+            b, c = divmod(rem, pk)
+            self.owner[(a, b, c)] = r
+        self.coord = next(k for k, v in self.owner.items() if v == rank)
+        a, b, c = self.coord
+        self.rows = split(M, pm, a)
+        self.cols = split(N, pn, b)
+        self.ks = split(K, pk, c)
+        mb, nb, kb = (self.rows[1] - self.rows[0], self.cols[1] - self.cols[0],
+                      self.ks[1] - self.ks[0])
+        self.mb, self.nb, self.kb = mb, nb, kb
+        # A[a, c] (mb x kb) and Bt[b, c] (nb x kb); my parts in place
+        self.A = torch.empty(mb, kb, dtype=torch.bfloat16, device=self.device)
+        self.Bt = torch.empty(nb, kb, dtype=torch.bfloat16, device=self.device)
+        ar = split(mb, pn, b)   # rows of A[a, c] I hold
+        bc = split(nb, pm, a)   # rows of Bt[b, c] (columns of B) I hold
+        self.A[ar[0]:ar[1]] = synth((self.rows[0] + ar[0], self.rows[0] + ar[1]), self.ks, K,
+                                    seed, self.device)
+        self.Bt[bc[0]:bc[1]] = synth((self.cols[0] + bc[0], self.cols[0] + bc[1]), self.ks, K,
+                                     seed + 1, self.device)
+        # C[a, b] rows owned after the reduce-scatter: k-group position c
+        self.my_rows = split(mb, pk, c)
+        crows = self.my_rows[1] - self.my_rows[0]
+        self.C = [torch.zeros(crows, nb, dtype=torch.float32, device=self.device)
+                  for _ in range(2)]
+        self.peers = PeerBuffers({"A": self.A, "Bt": self.Bt, "C0": self.C[0],
+                                  "C1": self.C[1]}, rank, world, group)
+        self.streams = [torch.cuda.Stream(device=self.device) for _ in range(4)]
+        # pulls: Bt parts from the m-group (other a'), A parts from the n-group (other b')
+        self.pulls = []
+        si = 0
+        for a2 in range(pm):
+            if a2 == a:
+                continue
+            r = split(nb, pm, a2)
+            self.pulls.append(("Bt", self.owner[(a2, b, c)], r, si % 4, torch.cuda.Event()))
+            si += 1
+        for b2 in range(pn):
+            if b2 == b:
+                continue
+            r = split(mb, pn, b2)
+            self.pulls.append(("A", self.owner[(a, b2, c)], r, si % 4, torch.cuda.Event()))
+            si += 1
+        # one GEMM per destination in the k-group; the local destination last
+        order = [(c + 1 + i) % pk for i in range(pk)]
+        self.gemms = [(split(mb, pk, d), self.owner[(a, b, d)]) for d in order]
+        self.done = torch.cuda.Event()
+        self.done.record()
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.step_i = 0
+        self.reduce = pk > 1
+        self.flops = 2 * mb * nb * kb
+        self.gemm_launches = len(self.gemms)
+        cb = comm_bytes_3d(M, N, K, self.grid)
+        self.recv_bytes = cb["total"]
+        self.comm = cb
+        self._dist = dist if world > 1 else None
+        torch.cuda.synchronize()
+        if self._dist:
+            dist.barrier(group=group)
+
+    def _barrier(self):
+        if self._dist:  # stream-ordered: NCCL runs after the queued GEMMs
+            self._dist.all_reduce(self.flag, group=self.group)
+
+    def step(self, stream=None):
+        torch = native.require_cuda()
+        from ..peer import copy2d
+
+        cs = stream or torch.cuda.current_stream()
+        buf = self.step_i % 2
+        self.step_i += 1
+        if self.reduce:
+            self.C[1 - buf].zero_()   # consumed: the previous step's result was in C[1-buf]
+            self._barrier()           # every GPU zeroed its C[buf] two steps ago and is here
+        for s in self.streams:
+            s.wait_event(self.done)
+        for name, q, (r0, r1), si, ev in self.pulls:
+            t = self.A if name == "A" else self.Bt
+            pitch = t.shape[1] * 2
+            off = r0 * pitch
+            copy2d(self.peers.ptrs[name][self.rank] + off, pitch, self.peers.ptrs[name][q] + off,
+                   pitch, pitch, r1 - r0, self.streams[si])
+            ev.record(self.streams[si])
+        for _, _, _, _, ev in self.pulls:
+            cs.wait_event(ev)
+        lib = native.lib()
+        for (r0, r1), dst in self.gemms:
+            cptr = self.peers.ptrs[f"C{buf}"][dst]
+            native.check(lib.pm_gemm_bf16(
+                self.A[r0:r1].data_ptr(), self.kb, self.Bt.data_ptr(), self.kb, cptr, self.nb,
+                r1 - r0, self.nb, self.kb, 0, 2 if self.reduce else 0, native.stream_ptr(cs)),
+                "pm_gemm_bf16")
+        self.done.record(cs)
+        return self.C[buf]
+
+    def result(self):
+        """This GPU's rows of C[a, b] after the last step (synchronises the peers)."""
+        if self.reduce:
+            self._barrier()
+        return self.C[(self.step_i - 1) % 2]
+
+    def close(self):
+        self.peers.close()
