@@ -263,6 +263,38 @@ def run_3d(args, rank, world, local, M, N, K, mapping):
     return res
 
 
+def run_stencil(args, rank, world, rows, cols, mapping, sweeps=20):
+    """BASELINE configs[4]: 5-point Jacobi fp32 with the fused NVLink halo exchange."""
+    import torch
+
+    from paper_2507_17087_b200.executors.stencil import MappedStencil
+
+    ex = MappedStencil(rows, cols, mapping=mapping, rank=rank, world=world, seed=7)
+    cs = torch.cuda.current_stream()
+    ex.run(3 * max(1, args.warmup))
+    torch.cuda.synchronize()
+    barrier(world)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(cs)
+    ex.run(sweeps)
+    t1.record(cs)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(t0.elapsed_time(t1) / sweeps, world)
+    _, _, hbm, _ = peaks()
+    cells = rows * cols
+    per_gpu_gbs = 8.0 * cells / world / (ms * 1e-3) / 1e9
+    res = {"grid": list(ex.grid), "ms_per_sweep": ms, "cells_per_s": cells / (ms * 1e-3),
+           "sweeps": sweeps, "bytes_per_cell": 8, "achieved_gbs_per_gpu": per_gpu_gbs,
+           "frac_hbm": per_gpu_gbs / hbm, "halo_cells_per_sweep": ex.halo_cells,
+           "halo_model_surface_volume": ex.model_halo,
+           "halo_bytes_per_sweep": 4 * (ex.halo_cells or 0)}
+    barrier(world)
+    ex.close()
+    del ex
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_e2e(args, ex, rank, world):
     """Same multiply through the public API with host buffers: H2D of this GPU's
     operand slices from pinned memory, the mapped multiply, D2H of its C block."""
@@ -401,6 +433,18 @@ def main_ours(args):
                         "comm_ratio": h["comm_bytes_per_gpu"]["total"] /
                         max(1, d["comm_bytes_per_gpu"]["total"])}
         extra["workloads_3d"] = wl
+    if not args.no_stencil:
+        st = {}
+        for name, (r, c) in (("square", (args.size, args.size)),
+                             ("aspect_1x4", (args.size // 2, 2 * args.size))):
+            d = run_stencil(args, rank, world, r, c, "decompose")
+            h = run_stencil(args, rank, world, r, c, "heuristic")
+            st[name] = {"rows": r, "cols": c, "decompose": d, "heuristic": h,
+                        "speedup": h["ms_per_sweep"] / d["ms_per_sweep"],
+                        "halo_ratio": (h["halo_cells_per_sweep"] or 1) /
+                        max(1, d["halo_cells_per_sweep"] or 1)}
+        extra["stencil"] = {"workload": "5-point Jacobi fp32, Mapple block mapping, fused NVLink "
+                                        "halo exchange (BASELINE configs[4])", **st}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         C64, dt, fl = cpu_sample(args)
@@ -535,6 +579,7 @@ def main():
     ap.add_argument("--no-kernels", action="store_true")
     ap.add_argument("--decompose-only", action="store_true")
     ap.add_argument("--no-3d", action="store_true", help="skip the Johnson / COSMA workloads")
+    ap.add_argument("--no-stencil", action="store_true", help="skip the stencil workload")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="host seconds spent on the CPU baseline sample")
     args = ap.parse_args()

@@ -163,6 +163,29 @@ int pm_ipc_close(void* base);
 int pm_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
                     int64_t height, void* stream);
 
+/* One 5-point Jacobi sweep of this GPU's rectangle of a block-mapped grid
+ * (the paper's stencil workload; ownership from the Mapple
+ * block mapping, halo totals = surface_volume, commvol.py:94-96).  Neighbour
+ * cells are read straight from the neighbours' `in` buffers (peer pointers);
+ * ordering with the neighbours uses flags each GPU pushes into the others'
+ * `my_flags` with system-scope release stores (see csrc/stencil.cu).  Three
+ * rotating buffers per GPU; `sweep` counts from 0. */
+typedef struct pm_stencil_view {
+  float* out;
+  const float* in;
+  int64_t rows, cols, pitch; /* my rectangle (elements) and its row pitch      */
+  int64_t grow0, gcol0;      /* global origin of the rectangle                 */
+  int64_t grows, gcols;      /* global extents                                 */
+  const float* nbr[4];       /* up, down, left, right neighbour `in` or NULL   */
+  int64_t nbr_pitch[4];
+  int64_t nbr_rows[4], nbr_cols[4];
+  int32_t* my_flags;         /* [world] sweep-done flags pushed by neighbours  */
+  int32_t* nbr_flag_slot[4]; /* &neighbour.my_flags[my rank] (peer pointers)   */
+  int32_t nbr_rank[4];
+  uint32_t* ticket;          /* cumulative CTA ticket (device, zero at start)  */
+} pm_stencil_view;
+int pm_stencil_sweep(const pm_stencil_view* view, int32_t sweep, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,183 @@
+// K5 -- 5-point Jacobi sweep of a block-mapped 2-D grid with the halo exchange
+// fused in (BASELINE configs[4]; the paper's stencil workload).
+//
+// Each GPU owns one rectangle of the global grid (from the Mapple block
+// mapping, K1 + K2).  A sweep reads buffer `in` and writes `out`:
+//   out[i][j] = 0.25 * (in[i-1][j] + in[i+1][j] + in[i][j-1] + in[i][j+1])
+// for interior cells of the global grid; global boundary cells are copied
+// (Dirichlet).  Cells just outside the rectangle are read straight from the
+// neighbouring GPU's `in` buffer over NVLink (peer pointers, L2-bypassing
+// loads) -- no halo buffers, no copies, no NCCL.
+//
+// Cross-GPU ordering, per neighbour (flags pushed into the reader's memory):
+//   RAW  a tile touching my rectangle's edge waits until that neighbour has
+//        finished the previous sweep (flag >= sweep); interior tiles do not;
+//   WAR  with three rotating buffers, a neighbour overwrites the buffer I
+//        read at sweep s only at its sweep s+2, so every tile just checks that
+//        neighbours finished sweep s-1 before writing (flag >= sweep - 1).
+// The last CTA of a sweep (cumulative atomic ticket) publishes "sweep done"
+// with a system-scope release store into each neighbour's flag array.
+// Tiles are launched interior-first so edge tiles usually find the flag set.
+//
+// Traffic: 8 B per cell per sweep from HBM (read in, write out); vertical
+// neighbours are reused through L1 inside a 16-row tile.
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pm_common.h"
+
+namespace pm {
+namespace {
+
+constexpr int TR = 16;    // rows per tile
+constexpr int TC = 512;   // cols per tile (128 threads x float4)
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(int32_t* p, int v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ float ld_peer(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void wait_flag(const int32_t* f, int target) {
+  if (ld_acquire_sys(f) >= target) return;
+  while (ld_acquire_sys(f) < target) __nanosleep(256);
+}
+
+// value of global cell (my-local coords i, j may be one step outside the rectangle)
+__device__ __forceinline__ float fetch(const pm_stencil_view& v, int64_t i, int64_t j) {
+  if (i >= 0 && i < v.rows && j >= 0 && j < v.cols) return __ldg(v.in + i * v.pitch + j);
+  if (i < 0) return ld_peer(v.nbr[0] + (v.nbr_rows[0] - 1) * v.nbr_pitch[0] + j);
+  if (i >= v.rows) return ld_peer(v.nbr[1] + j);
+  if (j < 0) return ld_peer(v.nbr[2] + i * v.nbr_pitch[2] + (v.nbr_cols[2] - 1));
+  return ld_peer(v.nbr[3] + i * v.nbr_pitch[3]);
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_interior) {
+  // interior tiles first, edge tiles last (block index order = launch order)
+  const int b = blockIdx.x;
+  int tr, tc;
+  if (b < n_interior) {
+    const int ic = tiles_c - 2;
+    tr = 1 + b / ic;
+    tc = 1 + b % ic;
+  } else {
+    // the ring of edge tiles: top row, bottom row, then left/right of the rest
+    int e = b - n_interior;
+    const int per_mid = tiles_c > 1 ? 2 : 1;
+    if (e < tiles_c) {
+      tr = 0;
+      tc = e;
+    } else if (tiles_r > 1 && e < 2 * tiles_c) {
+      tr = tiles_r - 1;
+      tc = e - tiles_c;
+    } else {
+      e -= (tiles_r > 1 ? 2 : 1) * tiles_c;
+      tr = 1 + e / per_mid;
+      tc = (e % per_mid == 0) ? 0 : tiles_c - 1;
+    }
+  }
+  const bool edge_r0 = tr == 0, edge_r1 = tr == tiles_r - 1;
+  const bool edge_c0 = tc == 0, edge_c1 = tc == tiles_c - 1;
+  const bool interior = !(edge_r0 || edge_r1 || edge_c0 || edge_c1);
+  if (threadIdx.x == 0) {
+    // WAR: neighbours must have finished sweep-1 before I overwrite `out`
+    for (int d = 0; d < 4; ++d)
+      if (v.nbr[d]) wait_flag(v.my_flags + v.nbr_rank[d], sweep - 1);
+    // RAW: edge tiles read neighbour cells produced by their sweep-1
+    const bool need[4] = {edge_r0, edge_r1, edge_c0, edge_c1};
+    for (int d = 0; d < 4; ++d)
+      if (v.nbr[d] && need[d]) wait_flag(v.my_flags + v.nbr_rank[d], sweep);
+  }
+  __syncthreads();
+
+  const int64_t r0 = (int64_t)tr * TR;
+  const int64_t c = (int64_t)tc * TC + threadIdx.x * 4;
+  if (interior && (v.pitch & 3) == 0) {
+    // all neighbours local and no global boundary: rolling float4 window
+    const float* p = v.in + (r0 - 1) * v.pitch + c;
+    float4 up = *reinterpret_cast<const float4*>(p);
+    float4 mid = *reinterpret_cast<const float4*>(p + v.pitch);
+#pragma unroll 4
+    for (int r = 0; r < TR; ++r) {
+      const float* row = p + (int64_t)(r + 1) * v.pitch;
+      const float4 dn = *reinterpret_cast<const float4*>(row + v.pitch);
+      const float lf = __ldg(row - 1), rt = __ldg(row + 4);
+      float4 o;
+      o.x = 0.25f * ((up.x + dn.x) + (lf + mid.y));
+      o.y = 0.25f * ((up.y + dn.y) + (mid.x + mid.z));
+      o.z = 0.25f * ((up.z + dn.z) + (mid.y + mid.w));
+      o.w = 0.25f * ((up.w + dn.w) + (mid.z + rt));
+      *reinterpret_cast<float4*>(v.out + (r0 + r) * v.pitch + c) = o;
+      up = mid;
+      mid = dn;
+    }
+  } else if (c < v.cols) {
+    const int64_t r1 = min(r0 + TR, v.rows);
+    const bool vec = (c + 4 <= v.cols) && ((v.pitch & 3) == 0);
+    for (int64_t i = r0; i < r1; ++i) {
+      const int64_t gi = v.grow0 + i;
+      float res[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t j = c + q;
+        if (j >= v.cols) { res[q] = 0.f; continue; }
+        const int64_t gj = v.gcol0 + j;
+        if (gi == 0 || gj == 0 || gi == v.grows - 1 || gj == v.gcols - 1) {
+          res[q] = __ldg(v.in + i * v.pitch + j);  // Dirichlet boundary
+        } else {
+          const float up = fetch(v, i - 1, j), dn = fetch(v, i + 1, j);
+          const float lf = fetch(v, i, j - 1), rt = fetch(v, i, j + 1);
+          res[q] = 0.25f * ((up + dn) + (lf + rt));
+        }
+      }
+      float* o = v.out + i * v.pitch + c;
+      if (vec) {
+        *reinterpret_cast<float4*>(o) = make_float4(res[0], res[1], res[2], res[3]);
+      } else {
+        for (int q = 0; q < 4 && c + q < v.cols; ++q) o[q] = res[q];
+      }
+    }
+  }
+  // publish "sweep done" once every CTA of this sweep has written its tile
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned total = gridDim.x;
+    const unsigned t = atomicAdd(v.ticket, 1u) + 1;
+    if (t == (unsigned)(sweep + 1) * total) {
+      __threadfence_system();
+      for (int d = 0; d < 4; ++d)
+        if (v.nbr[d]) st_release_sys(v.nbr_flag_slot[d], sweep + 1);
+    }
+  }
+}
+
+}  // namespace
+}  // namespace pm
+
+extern "C" int pm_stencil_sweep(const pm_stencil_view* v, int32_t sweep, void* stream) {
+  if (!v || !v->in || !v->out || v->rows <= 0 || v->cols <= 0 || v->pitch < v->cols || sweep < 0)
+    return pm::set_error("pm_stencil_sweep: bad view"), PM_ERR_INVALID;
+  const int tiles_r = (int)((v->rows + pm::TR - 1) / pm::TR);
+  const int tiles_c = (int)((v->cols + pm::TC - 1) / pm::TC);
+  const int n_interior = std::max(tiles_r - 2, 0) * std::max(tiles_c - 2, 0);
+  const int total = tiles_r * tiles_c;
+  pm::k_jacobi<<<total, pm::kThreads, 0, (cudaStream_t)stream>>>(*v, sweep, tiles_r, tiles_c,
+                                                                 n_interior);
+  PM_CUDA_TRY(cudaGetLastError());
+  return PM_OK;
+}

@@ -110,3 +110,6 @@ def stream_ptr(stream=None) -> int:
 
     s = stream if stream is not None else torch.cuda.current_stream()
     return int(s.cuda_stream)
+
+
+SIGNATURES["pm_stencil_sweep"] = (ctypes.c_int, [ctypes.c_void_p, _I32, _VP])

@@ -1,0 +1,53 @@
+"""Mapped stencil + 3-D matmul + peer-GEMM checks on the box's GPUs."""
+
+import json
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _ngpus():
+    import torch
+
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _run(script, n, port):
+    if n == 1:
+        cmd = [sys.executable, str(ROOT / "tests" / script)]
+    else:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+               str(ROOT / "tests" / script)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-4000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("{")][-1]
+    return json.loads(line)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+def test_stencil(n):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    v = _run("dist_stencil_check.py", n, 29700 + n)
+    assert v["ok"], v
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_grid3d(n):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    v = _run("dist_grid3d_check.py", n, 29710 + n)
+    assert v["ok"], v
+
+
+def test_peer_gemm_reduce_add():
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    v = _run("dist_peer_gemm_check.py", 2, 29720)
+    assert v["ok"], v
