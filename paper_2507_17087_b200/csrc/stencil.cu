@@ -24,14 +24,15 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "pm_common.h"
 
 namespace pm {
 namespace {
 
-constexpr int TR = 16;    // rows per tile
 constexpr int TC = 512;   // cols per tile (128 threads x float4)
 constexpr int kThreads = 128;
 
@@ -65,6 +66,7 @@ __device__ __forceinline__ float fetch(const pm_stencil_view& v, int64_t i, int6
   return ld_peer(v.nbr[3] + i * v.nbr_pitch[3]);
 }
 
+template <int TR>
 __global__ void __launch_bounds__(kThreads)
 k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_interior) {
   // interior tiles first, edge tiles last (block index order = launch order)
@@ -107,23 +109,86 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
   const int64_t r0 = (int64_t)tr * TR;
   const int64_t c = (int64_t)tc * TC + threadIdx.x * 4;
   if (interior && (v.pitch & 3) == 0) {
-    // all neighbours local and no global boundary: rolling float4 window
-    const float* p = v.in + (r0 - 1) * v.pitch + c;
-    float4 up = *reinterpret_cast<const float4*>(p);
-    float4 mid = *reinterpret_cast<const float4*>(p + v.pitch);
-#pragma unroll 4
-    for (int r = 0; r < TR; ++r) {
-      const float* row = p + (int64_t)(r + 1) * v.pitch;
-      const float4 dn = *reinterpret_cast<const float4*>(row + v.pitch);
-      const float lf = __ldg(row - 1), rt = __ldg(row + 4);
-      float4 o;
-      o.x = 0.25f * ((up.x + dn.x) + (lf + mid.y));
-      o.y = 0.25f * ((up.y + dn.y) + (mid.x + mid.z));
-      o.z = 0.25f * ((up.z + dn.z) + (mid.y + mid.w));
-      o.w = 0.25f * ((up.w + dn.w) + (mid.z + rt));
-      *reinterpret_cast<float4*>(v.out + (r0 + r) * v.pitch + c) = o;
-      up = mid;
-      mid = dn;
+    // all neighbours local and no global boundary: rolling float4 window,
+    // 8 rows of loads in flight per thread (in/out never alias)
+    const float* __restrict__ p = v.in + (r0 - 1) * v.pitch + c;
+    float* __restrict__ po = v.out + r0 * v.pitch + c;
+    const int64_t pitch = v.pitch;
+    float4 up = __ldg(reinterpret_cast<const float4*>(p));
+    float4 mid = __ldg(reinterpret_cast<const float4*>(p + pitch));
+    for (int r8 = 0; r8 < TR; r8 += 8) {
+      float4 dn[8];
+      float lf[8], rt[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float* row = p + (int64_t)(r8 + u + 1) * pitch;
+        dn[u] = __ldg(reinterpret_cast<const float4*>(row + pitch));
+        lf[u] = __ldg(row - 1);
+        rt[u] = __ldg(row + 4);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        float4 o;
+        o.x = 0.25f * ((up.x + dn[u].x) + (lf[u] + mid.y));
+        o.y = 0.25f * ((up.y + dn[u].y) + (mid.x + mid.z));
+        o.z = 0.25f * ((up.z + dn[u].z) + (mid.y + mid.w));
+        o.w = 0.25f * ((up.w + dn[u].w) + (mid.z + rt[u]));
+        __stcs(reinterpret_cast<float4*>(po + (int64_t)(r8 + u) * pitch), o);
+        up = mid;
+        mid = dn[u];
+      }
+    }
+  } else if ((v.pitch & 3) == 0 && c + 4 <= v.cols) {
+    // edge tile, full vector: same rolling window, rows / columns just outside
+    // the rectangle come from the neighbours over NVLink
+    auto row4 = [&](int64_t i) -> float4 {
+      if (i >= 0 && i < v.rows) return *reinterpret_cast<const float4*>(v.in + i * v.pitch + c);
+      const float* q = nullptr;
+      if (i < 0 && v.nbr[0]) q = v.nbr[0] + (v.nbr_rows[0] - 1) * v.nbr_pitch[0] + c;
+      if (i >= v.rows && v.nbr[1]) q = v.nbr[1] + c;
+      if (!q) return make_float4(0.f, 0.f, 0.f, 0.f);  // global boundary: unused
+      return make_float4(ld_peer(q), ld_peer(q + 1), ld_peer(q + 2), ld_peer(q + 3));
+    };
+    const int64_t r1 = min(r0 + TR, v.rows);
+    float4 up = row4(r0 - 1), mid = row4(r0);
+    const bool g_first = v.gcol0 + c == 0, g_last = v.gcol0 + c + 3 == v.gcols - 1;
+    for (int64_t i8 = r0; i8 < r1; i8 += 8) {
+      // issue the batch's loads first (peer loads included) so their NVLink
+      // latencies overlap instead of serialising row by row
+      float4 dn[8];
+      float lf[8], rt[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t i = i8 + u;
+        dn[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        lf[u] = rt[u] = 0.f;
+        if (i >= r1) continue;
+        dn[u] = row4(i + 1);
+        if (c > 0) lf[u] = __ldg(v.in + i * v.pitch + c - 1);
+        else if (v.nbr[2]) lf[u] = ld_peer(v.nbr[2] + i * v.nbr_pitch[2] + (v.nbr_cols[2] - 1));
+        if (c + 4 < v.cols) rt[u] = __ldg(v.in + i * v.pitch + c + 4);
+        else if (v.nbr[3]) rt[u] = ld_peer(v.nbr[3] + i * v.nbr_pitch[3]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t i = i8 + u;
+        if (i >= r1) break;
+        float4 o;
+        o.x = 0.25f * ((up.x + dn[u].x) + (lf[u] + mid.y));
+        o.y = 0.25f * ((up.y + dn[u].y) + (mid.x + mid.z));
+        o.z = 0.25f * ((up.z + dn[u].z) + (mid.y + mid.w));
+        o.w = 0.25f * ((up.w + dn[u].w) + (mid.z + rt[u]));
+        const int64_t gi = v.grow0 + i;
+        if (gi == 0 || gi == v.grows - 1) {
+          o = mid;  // Dirichlet rows
+        } else {
+          if (g_first) o.x = mid.x;  // Dirichlet columns
+          if (g_last) o.w = mid.w;
+        }
+        __stcs(reinterpret_cast<float4*>(v.out + i * v.pitch + c), o);
+        up = mid;
+        mid = dn[u];
+      }
     }
   } else if (c < v.cols) {
     const int64_t r1 = min(r0 + TR, v.rows);
@@ -153,6 +218,7 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
     }
   }
   // publish "sweep done" once every CTA of this sweep has written its tile
+  if (!(v.nbr[0] || v.nbr[1] || v.nbr[2] || v.nbr[3])) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -172,12 +238,22 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
 extern "C" int pm_stencil_sweep(const pm_stencil_view* v, int32_t sweep, void* stream) {
   if (!v || !v->in || !v->out || v->rows <= 0 || v->cols <= 0 || v->pitch < v->cols || sweep < 0)
     return pm::set_error("pm_stencil_sweep: bad view"), PM_ERR_INVALID;
-  const int tiles_r = (int)((v->rows + pm::TR - 1) / pm::TR);
+  static int tr_env = [] {
+    const char* e = getenv("PM_STENCIL_TR");
+    return e ? atoi(e) : 16;
+  }();
+  const int TR = (tr_env == 32 || tr_env == 64 || tr_env == 128) ? tr_env : 16;
+  const int tiles_r = (int)((v->rows + TR - 1) / TR);
   const int tiles_c = (int)((v->cols + pm::TC - 1) / pm::TC);
   const int n_interior = std::max(tiles_r - 2, 0) * std::max(tiles_c - 2, 0);
   const int total = tiles_r * tiles_c;
-  pm::k_jacobi<<<total, pm::kThreads, 0, (cudaStream_t)stream>>>(*v, sweep, tiles_r, tiles_c,
-                                                                 n_interior);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (TR) {
+    case 16: pm::k_jacobi<16><<<total, pm::kThreads, 0, s>>>(*v, sweep, tiles_r, tiles_c, n_interior); break;
+    case 32: pm::k_jacobi<32><<<total, pm::kThreads, 0, s>>>(*v, sweep, tiles_r, tiles_c, n_interior); break;
+    case 128: pm::k_jacobi<128><<<total, pm::kThreads, 0, s>>>(*v, sweep, tiles_r, tiles_c, n_interior); break;
+    default: pm::k_jacobi<64><<<total, pm::kThreads, 0, s>>>(*v, sweep, tiles_r, tiles_c, n_interior); break;
+  }
   PM_CUDA_TRY(cudaGetLastError());
   return PM_OK;
 }

@@ -178,12 +178,19 @@ class MappedStencil:
         """`sweeps` Jacobi sweeps, stream-ordered; returns this GPU's current block."""
         lib = native.lib()
         sp = native.stream_ptr(stream)
+        if not hasattr(self, "_views"):  # the three buffer rotations, built once
+            self._views = [ctypes.byref(self._keep(self._view(s))) for s in range(3)]
+        fn = lib.pm_stencil_sweep
         for _ in range(sweeps):
-            v = self._view(self.sweep)
-            native.check(lib.pm_stencil_sweep(ctypes.byref(v), self.sweep, sp),
-                         "pm_stencil_sweep")
+            rc = fn(self._views[self.sweep % 3], self.sweep, sp)
+            if rc:
+                native.check(rc, "pm_stencil_sweep")
             self.sweep += 1
         return self.current()
+
+    def _keep(self, v):
+        self.__dict__.setdefault("_view_objs", []).append(v)
+        return v
 
     def current(self):
         return self.buf[self.sweep % 3][:, :self.mc]
