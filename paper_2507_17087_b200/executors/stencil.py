@@ -79,6 +79,28 @@ def rectangles_from_owner(ids, rows: int, cols: int, world: int, counts):
     return rects
 
 
+def block_neighbors(rects, rank: int, rows: int, cols: int) -> list:
+    """[up, down, left, right] neighbour ranks of a 2-D block grid (None at the
+    global boundary); raises unless every internal edge has exactly one owner."""
+    r0, r1, c0, c1 = rects[rank]
+    nbrs = [None] * 4
+    for q, (q0, q1, p0, p1) in enumerate(rects):
+        if q == rank:
+            continue
+        if (p0, p1) == (c0, c1) and q1 == r0:
+            nbrs[0] = q
+        elif (p0, p1) == (c0, c1) and q0 == r1:
+            nbrs[1] = q
+        elif (q0, q1) == (r0, r1) and p1 == c0:
+            nbrs[2] = q
+        elif (q0, q1) == (r0, r1) and p0 == c1:
+            nbrs[3] = q
+    for d, (lo, hi) in enumerate(((r0, 0), (r1, rows), (c0, 0), (c1, cols))):
+        if lo != hi and nbrs[d] is None:
+            raise ValueError("the mapping is not a 2-D block grid (missing neighbour)")
+    return nbrs
+
+
 def init_grid(rows: tuple, cols: tuple, ld: int, seed: int, device):
     """Deterministic U(0, 1) fp32 block of a virtual [*, ld] grid."""
     torch = native.require_cuda()
@@ -129,22 +151,7 @@ class MappedStencil:
         names = {f"b{i}": b for i, b in enumerate(self.buf)}
         names["flags"] = self.flags
         self.peers = PeerBuffers(names, rank, world, group)
-        # neighbours of a block grid: the owner just outside each edge
-        self.nbrs = [None] * 4
-        for q, (q0, q1, p0, p1) in enumerate(self.rects):
-            if q == rank:
-                continue
-            if (p0, p1) == (c0, c1) and q1 == r0:
-                self.nbrs[0] = q
-            elif (p0, p1) == (c0, c1) and q0 == r1:
-                self.nbrs[1] = q
-            elif (q0, q1) == (r0, r1) and p1 == c0:
-                self.nbrs[2] = q
-            elif (q0, q1) == (r0, r1) and p0 == c1:
-                self.nbrs[3] = q
-        for d, (lo, hi, pos) in enumerate(((r0, 0, 0), (r1, rows, 0), (c0, 0, 1), (c1, cols, 1))):
-            if lo != hi and self.nbrs[d] is None:
-                raise ValueError("the mapping is not a 2-D block grid (missing neighbour)")
+        self.nbrs = block_neighbors(self.rects, rank, rows, cols)
         self.sweep = 0
         self.torch = torch
         self._dist = dist if world > 1 else None

@@ -153,6 +153,76 @@ def synth(rows: tuple, cols: tuple, ld: int, seed: int, device):
     return ((x.to(torch.float32) / float(1 << 30)) - 1.0).to(torch.bfloat16)
 
 
+@dataclass(frozen=True)
+class PanelPlan:
+    panels: list      # (k0, k1, A source rank, B source rank), in execution order
+    chunks: list      # A row chunks of remote panels
+    pulls: list       # (operand, source rank, row0, rows, k0, k1, stream index)
+    gemms: list       # (r0, r1, k0, k1, accumulate, [indices into pulls to wait for])
+    n_streams: int
+
+
+def plan_panels(layout: Layout, me: int, K: int, mr: int, nc: int, block: int = 128,
+                a_chunks: int = 4, copy_streams: int = 4) -> PanelPlan:
+    """The per-GPU SUMMA schedule (pure; CPU-testable).
+
+    K is cut at every slice boundary of my row group (A) and column group (B),
+    so on each panel both operands come from single GPUs.  Panels whose
+    operands are both local run first -- no waiting -- while the copy engines
+    bring in the others; remote panels are split into row chunks of A so the
+    GEMM of chunk c overlaps the pull of chunk c+1.  The first panel writes C,
+    later ones accumulate (TMA reduce-add epilogue).
+    """
+    cuts = {0, K}
+    for q in layout.row_group[me]:
+        cuts.update(layout.a_slice[q])
+    for q in layout.col_group[me]:
+        cuts.update(layout.b_slice[q])
+    cuts = sorted(cuts)
+    ranked = []
+    for k0, k1 in zip(cuts, cuts[1:]):
+        if k1 <= k0:
+            continue
+        a_src = next(q for q in layout.row_group[me]
+                     if layout.a_slice[q][0] <= k0 and k1 <= layout.a_slice[q][1])
+        b_src = next(q for q in layout.col_group[me]
+                     if layout.b_slice[q][0] <= k0 and k1 <= layout.b_slice[q][1])
+        remote = (a_src != me) * mr * (k1 - k0) + (b_src != me) * nc * (k1 - k0)
+        ranked.append((remote, k0, k1, a_src, b_src))
+    ranked.sort()
+    nbr = -(-mr // block)
+    n = max(1, min(a_chunks, nbr))
+    chunks = [(min(mr, nbr * c // n * block), min(mr, nbr * (c + 1) // n * block))
+              for c in range(n)]
+    chunks = [(a, b) for a, b in chunks if b > a]
+    n_streams = copy_streams if any(r[0] for r in ranked) else 0
+    pulls, gemms = [], []
+    rr = 0
+
+    def pull(name, q, row0, rows, k0, k1):
+        nonlocal rr
+        idx = []
+        pieces = min(n_streams, max(1, rows // block))
+        for i in range(pieces):
+            a = row0 + rows * i // pieces
+            b = row0 + rows * (i + 1) // pieces
+            pulls.append((name, q, a, b - a, k0, k1, rr % n_streams))
+            idx.append(len(pulls) - 1)
+            rr += 1
+        return idx
+
+    first = True
+    for _, k0, k1, a_src, b_src in ranked:
+        b_evs = pull("Bt", b_src, 0, nc, k0, k1) if b_src != me else []
+        for r0, r1 in (chunks if a_src != me else [(0, mr)]):
+            a_evs = pull("A", a_src, r0, r1 - r0, k0, k1) if a_src != me else []
+            gemms.append((r0, r1, k0, k1, not first, b_evs + a_evs))
+            b_evs = []  # later chunks of this panel run after the first on one stream
+        first = False
+    return PanelPlan([(k0, k1, a, b) for _, k0, k1, a, b in ranked], chunks, pulls, gemms,
+                     n_streams)
+
+
 class MappedGemm:
     """One GPU's share of a mapped SUMMA multiply (see module docstring)."""
 
@@ -198,68 +268,18 @@ class MappedGemm:
     # -- schedule (built once) -------------------------------------------------------
 
     def _plan(self, block, a_chunks, copy_streams):
-        """K panels ordered by how much of them is local, then pulls per panel.
-
-        A panel is a K-range on which both operands each come from a single GPU
-        (mine or a peer of my row / column group).  Panels whose operands are
-        both local are multiplied first -- no waiting -- while the copy engines
-        bring in the others; remote panels are split into row chunks of A so the
-        GEMM of chunk c overlaps the pull of chunk c+1.  The first panel writes
-        C, later panels accumulate into it (TMA reduce-add epilogue).
-        """
+        """Bind the pure schedule (`plan_panels`) to CUDA streams and events."""
         torch = native.require_cuda()
-        lay, me, K = self.layout, self.rank, self.K
         mr, nc = self.rows[1] - self.rows[0], self.cols[1] - self.cols[0]
-        cuts = {0, K}
-        for q in lay.row_group[me]:
-            cuts.update(lay.a_slice[q])
-        for q in lay.col_group[me]:
-            cuts.update(lay.b_slice[q])
-        cuts = sorted(cuts)
-        panels = []
-        for k0, k1 in zip(cuts, cuts[1:]):
-            if k1 <= k0:
-                continue
-            a_src = next(q for q in lay.row_group[me] if lay.a_slice[q][0] <= k0 and k1 <= lay.a_slice[q][1])
-            b_src = next(q for q in lay.col_group[me] if lay.b_slice[q][0] <= k0 and k1 <= lay.b_slice[q][1])
-            remote = (a_src != me) * mr * (k1 - k0) + (b_src != me) * nc * (k1 - k0)
-            panels.append((remote, k0, k1, a_src, b_src))
-        panels.sort()
-        nbr = -(-mr // block)
-        n = max(1, min(a_chunks, nbr))
-        chunks = [(min(mr, nbr * c // n * block), min(mr, nbr * (c + 1) // n * block))
-                  for c in range(n)]
-        chunks = [(a, b) for a, b in chunks if b > a]
-        any_remote = any(p[0] for p in panels)
-        self.copy_streams = ([torch.cuda.Stream(device=self.device) for _ in range(copy_streams)]
-                             if any_remote else [])
-        self.pulls = []   # (name, src rank, row0, rows, k0, k1, stream index, event)
-        self.gemms = []   # (r0, r1, k0, k1, accumulate, [events to wait for])
-        first = True
-        rr = 0
-
-        def pull(name, q, row0, rows, k0, k1):
-            nonlocal rr
-            evs = []
-            pieces = min(len(self.copy_streams), max(1, rows // block))
-            for i in range(pieces):
-                a = row0 + rows * i // pieces
-                b = row0 + rows * (i + 1) // pieces
-                ev = torch.cuda.Event()
-                self.pulls.append((name, q, a, b - a, k0, k1, rr % len(self.copy_streams), ev))
-                rr += 1
-                evs.append(ev)
-            return evs
-
-        for _, k0, k1, a_src, b_src in panels:
-            b_evs = pull("Bt", b_src, 0, nc, k0, k1) if b_src != me else []
-            for r0, r1 in (chunks if a_src != me else [(0, mr)]):
-                a_evs = pull("A", a_src, r0, r1 - r0, k0, k1) if a_src != me else []
-                self.gemms.append((r0, r1, k0, k1, not first, b_evs + a_evs))
-                b_evs = []  # later chunks of this panel are ordered after the first
-            first = False
-        self.panels = [(k0, k1, a_src, b_src) for _, k0, k1, a_src, b_src in panels]
-        self.chunks = chunks
+        plan = plan_panels(self.layout, self.rank, self.K, mr, nc, block, a_chunks, copy_streams)
+        self.copy_streams = [torch.cuda.Stream(device=self.device)
+                             for _ in range(plan.n_streams)]
+        events = [torch.cuda.Event() for _ in plan.pulls]
+        self.pulls = [p + (events[i],) for i, p in enumerate(plan.pulls)]
+        self.gemms = [(r0, r1, k0, k1, acc, [events[i] for i in evs])
+                      for r0, r1, k0, k1, acc, evs in plan.gemms]
+        self.panels = plan.panels
+        self.chunks = plan.chunks
 
     # -- one multiply ---------------------------------------------------------------
 
