@@ -21,13 +21,20 @@ struct ProcKey {
   const int* __restrict__ proc;
   int nbins;
   unsigned long long* bad;
-  __device__ __forceinline__ int operator()(long long i) const {
-    const int b = __ldg(proc + i);
+  bool vec_ok;  // proc is 16-byte aligned: keys4() may use vector loads
+  __device__ __forceinline__ int check(int b, long long i) const {
     if (b < 0 || b >= nbins) {
       atomicMin(bad, (unsigned long long)i);
       return -1;
     }
     return b;
+  }
+  __device__ __forceinline__ int operator()(long long i) const { return check(__ldg(proc + i), i); }
+  // four consecutive ids (i % 4 == 0) packed as int8 bins
+  __device__ __forceinline__ int keys4(long long i) const {
+    const int4 v = __ldg(reinterpret_cast<const int4*>(proc + i));
+    return (check(v.x, i) & 0xFF) | ((check(v.y, i + 1) & 0xFF) << 8) |
+           ((check(v.z, i + 2) & 0xFF) << 16) | ((check(v.w, i + 3) & 0xFF) << 24);
   }
 };
 
@@ -56,7 +63,8 @@ int pm_partition(const int32_t* proc, int64_t n, int32_t nbins, int64_t* counts,
     return pm::set_error("pm_partition: int32 permutation needs n < 2^31"), PM_ERR_UNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
   PM_CUDA_TRY(cudaMemsetAsync(bad, 0xFF, sizeof(int64_t), s));
-  pm::ProcKey key{proc, nbins, reinterpret_cast<unsigned long long*>(bad)};
+  pm::ProcKey key{proc, nbins, reinterpret_cast<unsigned long long*>(bad),
+                  ((uintptr_t)proc % 16) == 0};
   pm::PermSink sink{perm};
   return pm::stable_partition(key, sink, perm != nullptr, n, nbins,
                               reinterpret_cast<long long*>(counts),
