@@ -152,6 +152,7 @@ struct Params {
   int group_m;  // tile raster: group_m M-tiles advance together across N
   int debug_nostore;  // experiments only (PM_GEMM_NOSTORE): skip the C stores
   int tma_store;      // epilogue through smem + TMA bulk store (map_c valid)
+  int* tile_counter;  // dynamic tile scheduler ticket (zeroed before each launch)
 };
 
 __device__ __forceinline__ void tile_coords(int t, const Params& p, int& tm, int& tn) {
@@ -622,6 +623,23 @@ constexpr int kEpiWarps = 8;
 constexpr int SMEMW = kStagesW * STAGEW + kEpiWarps * EPI_BUF + 1024 + 512;
 constexpr int WM = 512, WN = 256;
 constexpr int kThreadsW = 384;  // warps 0-3 control, 4-7 drain half 0, 8-11 drain half 1
+constexpr int kQ = 4;           // tile-queue slots
+// consumers of every tile-queue slot: the non-leader producer, the leader's
+// MMA thread and the 8 epilogue warps of each CTA
+constexpr int kQConsumers = 1 + 1 + 2 * kEpiWarps;
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, 10000000;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
 
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -751,7 +769,10 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
   uint64_t* empty = bars + kStagesW;        // per CTA (leader's commit)
   uint64_t* tfull = bars + 2 * kStagesW;    // per CTA (leader's commit)
   uint64_t* tempty = bars + 2 * kStagesW + 1;  // [2] leader's, count 8 each
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kStagesW + 3);
+  uint64_t* qfull = bars + 2 * kStagesW + 3;   // [kQ] per CTA: tile index published
+  uint64_t* qempty = qfull + kQ;               // [kQ] leader's: all consumers read it
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(qempty + kQ);
+  int* tileq = reinterpret_cast<int*>(tmem_holder + 4);  // [kQ] tile ring
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -775,6 +796,10 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
     mbar_init(&tfull[0], 1);
     mbar_init(&tempty[0], 8);
     mbar_init(&tempty[1], 8);
+    for (int i = 0; i < kQ; ++i) {
+      mbar_init(&qfull[i], 1);
+      mbar_init(&qempty[i], kQConsumers);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -787,6 +812,37 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+
+  // Dynamic tile scheduler: the leader's producer draws tiles from a global
+  // ticket and publishes them through a kQ-slot ring in both CTAs; every role
+  // of both CTAs walks the same sequence.  Tiles therefore run in raster order
+  // of their start time, so the tiles resident at any moment stay contiguous
+  // in the grouped raster and share A/B panels in L2 -- with a static
+  // round-robin the pairs drift apart over ~100 waves and L2 reuse collapses
+  // (ncu: 211 GB DRAM reads for one 32768^3 launch).
+  const uint32_t qempty0 = mapa_shared(smem_u32(&qempty[0]), 0);
+  int q_slot = 0;
+  uint32_t q_phase = 0;
+  auto next_tile = [&]() -> int {  // consumers: wait, read, release the slot
+    mbar_wait_cluster(&qfull[q_slot], q_phase);
+    const int t = *(volatile int*)&tileq[q_slot];
+    mbar_arrive_cluster(qempty0 + q_slot * 8);
+    if (++q_slot == kQ) { q_slot = 0; q_phase ^= 1; }
+    return t;
+  };
+  auto publish_tile = [&]() -> int {  // leader producer: draw and publish
+    mbar_wait(&qempty[q_slot], q_phase ^ 1);
+    const int t = atomicAdd(p.tile_counter, 1);
+    tileq[q_slot] = t;
+    const uint32_t peer_q = mapa_shared(smem_u32(&tileq[q_slot]), 1);
+    asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(peer_q), "r"(t) : "memory");
+    mbar_arrive(&qfull[q_slot]);
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                     mapa_shared(smem_u32(&qfull[q_slot]), 1))
+                 : "memory");
+    if (++q_slot == kQ) { q_slot = 0; q_phase ^= 1; }
+    return t;
+  };
 
   auto coords = [&](int t, int& tm, int& tn) {
     const int per_group = p.group_m * tiles_n;
@@ -803,7 +859,9 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
       const uint32_t full0 = mapa_shared(smem_u32(&full[0]), 0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < ntiles; t += npairs) {
+      for (;;) {
+        const int t = leader ? publish_tile() : next_tile();
+        if (t >= ntiles) break;
         int tm, tn;
         coords(t, tm, tn);
         const int am = tm * WM + crank * 128;
@@ -829,8 +887,8 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
       constexpr uint32_t idesc = make_idesc(256, WN);
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int t = pair; t < ntiles; t += npairs, ++it) {
+      for (int it = 0;; ++it) {
+        if (next_tile() >= ntiles) break;
         const uint32_t tphase = it & 1;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
@@ -859,8 +917,11 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
     const int h = (warp - 4) >> 2;  // TMEM half drained by this warp
     const int q = warp & 3;         // TMEM lane quarter this warp may access
     const uint32_t tempty_h = mapa_shared(smem_u32(&tempty[h]), 0);
-    int it = 0;
-    for (int t = pair; t < ntiles; t += npairs, ++it) {
+    for (int it = 0;; ++it) {
+      int t = 0;
+      if (lane == 0) t = next_tile();
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= ntiles) break;
       int tm, tn;
       coords(t, tm, tn);
       mbar_wait(&tfull[0], it & 1);
@@ -958,7 +1019,10 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
   p.c16 = c_bf16 ? reinterpret_cast<__nv_bfloat16*>(C) : nullptr;
   p.ldc = ldc;
   p.accumulate = accumulate != 0;
-  p.group_m = kind == 2 ? 6 : 8;
+  // raster group (M-tiles per group): long K panels do not fit L2, so narrow
+  // groups re-read less from HBM (sustained sweep: K=32768 g2 1270 TF/s vs g6
+  // 1151; K=16384 g4 best)
+  p.group_m = kind == 2 ? (K >= 24576 ? 2 : 4) : 8;
   if (const char* g = getenv("PM_GEMM_GROUP")) p.group_m = atoi(g) > 0 ? atoi(g) : p.group_m;
   p.debug_nostore = getenv("PM_GEMM_NOSTORE") ? 1 : 0;
   static bool attr_done[64] = {false};
@@ -1024,6 +1088,13 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
         if (r != CUDA_SUCCESS)
           return pm::set_error("cuTensorMapEncodeTiled(C) failed: %d", (int)r), PM_ERR_CUDA;
       }
+      // tile-scheduler ticket: a ring of 64 counters per device (library
+      // scratch), zeroed on the launch stream
+      static int* counters[64] = {nullptr};
+      static unsigned next_slot[64] = {0};
+      if (!counters[dev]) PM_CUDA_TRY(cudaMalloc(&counters[dev], 64 * 128));
+      p.tile_counter = counters[dev] + (next_slot[dev]++ % 64) * 32;
+      PM_CUDA_TRY(cudaMemsetAsync(p.tile_counter, 0, sizeof(int), (cudaStream_t)stream));
       wide::k_gemm_bf16_wide<<<(unsigned)(2 * pairs), wide::kThreadsW, wide::SMEMW,
                                (cudaStream_t)stream>>>(ma, mb, mc, p);
     } else {
