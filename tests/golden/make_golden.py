@@ -312,7 +312,60 @@ def shard_cases():
     return out
 
 
+def cli_cases():
+    """The reference CLI's exact stdout and exit code (cli.py:358-435)."""
+    import contextlib
+    import io
+    import tempfile
+
+    from procmap.cli import main as ref_main
+
+    corpus = {p.stem: p.read_text() for p in CORPUS.glob("*.mapper")}
+    plans = [
+        ("map", "block2d_full", ["--task", "loop0", "--ispace", "6,6", "--machine", "2x2"]),
+        ("map", "matmul_mappers", ["--task", "cannon_mm", "--ispace", "4,4", "--machine", "2x4"]),
+        ("map", "matmul_mappers", ["--task", "solomonik_mm", "--ispace", "4,4,4", "--machine",
+                                   "2x4"]),
+        ("map", "distributions", ["--task", "t_cyclic2D", "--ispace", "5,3", "--format", "csv"]),
+        ("map", "linear_cyclic", ["--task", "loop0", "--ispace", "7,2", "--machine", "1x8"]),
+        ("map", "block2d_full", ["--task", "nosuchtask", "--ispace", "2,2"]),
+        ("parse", "matmul_mappers", []),
+        ("parse", "block2d_full", ["--format", "csv"]),
+        ("decompose", None, ["6", "--extents", "12,18"]),
+        ("decompose", None, ["8", "--extents", "65536,16384,16384"]),
+        ("decompose", None, ["16", "--extents", "4,8,4", "--objective", "halo", "--halo", "1,2,1"]),
+        ("decompose", None, ["8", "--extents", "12,18", "--strict"]),
+        ("commvol", None, ["--extents", "12,18", "--grid", "3,2"]),
+        ("commvol", None, ["--extents", "4,8,4", "--grid", "2,4,2", "--transpose-dims", "1",
+                           "--halo", "1,0,2"]),
+        ("sweep", None, []),
+        ("sweep", None, ["--ratios", "1,4", "--areas", "1000000", "--gpus", "8,16",
+                         "--format", "csv"]),
+    ]
+    out = []
+    for cmd, mapper, rest in plans:
+        argv = [cmd]
+        path = None
+        if mapper:
+            fh = tempfile.NamedTemporaryFile("w", suffix=".mapper", delete=False)
+            fh.write(corpus[mapper])
+            fh.close()
+            path = fh.name
+            argv.append(path)
+        argv += rest
+        buf, err = io.StringIO(), io.StringIO()
+        with contextlib.redirect_stdout(buf), contextlib.redirect_stderr(err):
+            code = ref_main(argv)
+        text = buf.getvalue()
+        if path:
+            text = text.replace(path, "@MAPPER@")
+        out.append({"cmd": cmd, "mapper": mapper, "source": corpus.get(mapper), "args": rest,
+                    "stdout": text, "exit": code})
+    return out
+
+
 def main():
+    (OUT / "cli.json").write_text(json.dumps(cli_cases(), separators=(",", ":")))
     mapping = mapping_cases()
     sources = sorted({c["source"] for c in mapping})
     index = {s: i for i, s in enumerate(sources)}
