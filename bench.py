@@ -263,6 +263,42 @@ def run_3d(args, rank, world, local, M, N, K, mapping):
     return res
 
 
+def run_cannon(args, rank, world, N, layers, dtype):
+    """BASELINE configs[0] (Cannon fp32 N=1024 on 2x2) and the Cannon / 2.5D
+    bf16 variants: Cannon skew + shifts as NVLink pulls, 2.5D layer reduction
+    fused into the GEMM epilogue."""
+    import torch
+
+    from paper_2507_17087_b200.executors.cannon import MappedCannon, cannon_moves
+
+    ex = MappedCannon(N, layers=layers, rank=rank, world=world, dtype=dtype, seed=31)
+    cs = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        ex.step()
+    ex.result()
+    torch.cuda.synchronize()
+    barrier(world)
+    steps = max(3, args.steps // 2)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(cs)
+    for _ in range(steps):
+        ex.step()
+    ex.result()
+    t1.record(cs)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(t0.elapsed_time(t1) / steps, world)
+    moves = int(sum_over_ranks(ex.moved_blocks, world))
+    res = {"N": N, "dtype": dtype, "grid": [ex.q, ex.q, ex.c], "machine": list(ex.machine),
+           "ms_per_multiply": ms, "tflops": 2.0 * N ** 3 / (ms * 1e-3) / 1e12,
+           "block_moves": moves, "block_moves_schedule": cannon_moves(ex.q, ex.c),
+           "bytes_moved": moves * ex.block_bytes}
+    barrier(world)
+    ex.close()
+    del ex
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_stencil(args, rank, world, rows, cols, mapping, sweeps=20):
     """BASELINE configs[4]: 5-point Jacobi fp32 with the fused NVLink halo exchange."""
     import torch
@@ -494,6 +530,14 @@ def main_ours(args):
                         "comm_ratio": h["comm_bytes_per_gpu"]["total"] /
                         max(1, d["comm_bytes_per_gpu"]["total"])}
         extra["workloads_3d"] = wl
+    if not args.no_cannon:
+        cn = {}
+        if world in (1, 4):  # q x q grids: configs[0] is Cannon fp32 N=1024 on 2x2
+            cn["cannon_fp32_N1024"] = run_cannon(args, rank, world, 1024, 1, "fp32")
+            cn["cannon_bf16"] = run_cannon(args, rank, world, args.size, 1, "bf16")
+        if world == 8:       # configs[2]: Solomonik 2.5D on 2x2x2
+            cn["solomonik_2p5d_bf16"] = run_cannon(args, rank, world, args.size, 2, "bf16")
+        extra["cannon"] = cn
     if not args.no_stencil:
         st = {}
         for name, (r, c) in (("square", (args.size, args.size)),
@@ -641,6 +685,7 @@ def main():
     ap.add_argument("--decompose-only", action="store_true")
     ap.add_argument("--no-3d", action="store_true", help="skip the Johnson / COSMA workloads")
     ap.add_argument("--no-stencil", action="store_true", help="skip the stencil workload")
+    ap.add_argument("--no-cannon", action="store_true", help="skip the Cannon / 2.5D workloads")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="host seconds spent on the CPU baseline sample")
     args = ap.parse_args()

@@ -150,6 +150,12 @@ int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t ldb, void* 
                  int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t c_bf16,
                  int32_t accumulate, void* stream);
 
+/* Same on fp32 operands through the TF32 tensor-core path (tcgen05 kind::tf32,
+ * fp32 accumulation): A[M,K], Bt[N,K], C[M,N] fp32 row-major; lda, ldb % 4 == 0.
+ * Used for the fp32 Cannon configuration (BASELINE configs[0]). */
+int pm_gemm_tf32(const float* A, int64_t lda, const float* Bt, int64_t ldb, float* C, int64_t ldc,
+                 int64_t M, int64_t N, int64_t K, int32_t accumulate, void* stream);
+
 /* NVLink peer memory for the mapped executors (replaces the Legion/Realm
  * data movement the paper's runs used; the reference
  * package models it only as element counts, commvol.py:1-17).

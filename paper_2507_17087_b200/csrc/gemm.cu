@@ -122,6 +122,23 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
   return d;
 }
 
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// kind::tf32 instruction descriptor: D=f32, A=B=tf32 (format 2), both K-major.
+__host__ __device__ constexpr uint32_t make_idesc_tf32(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(m >> 4) << 24);
+}
+
 // kind::f16 instruction descriptor: D=f32, A=B=bf16, both K-major.
 __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
@@ -166,9 +183,13 @@ __device__ __forceinline__ void tile_coords(int t, const Params& p, int& tm, int
   tn = r / gm;
 }
 
+// TF32 = true: fp32 operands on the tensor cores (kind::tf32, 32 fp32 = one
+// 128-byte swizzle row per k-block, UMMA K = 8); same smem bytes per stage.
+template <bool TF32>
 __global__ void __launch_bounds__(kThreads, 1)
-k_gemm_bf16(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-            const Params p) {
+k_gemm_1sm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+           const Params p) {
+  constexpr int BKE = TF32 ? 32 : BK;  // elements per 128-byte k-block row
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -221,15 +242,15 @@ k_gemm_bf16(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(&map_a, &full[stage], sa + stage * A_BYTES, kb * BK, tm * BM);
-          tma_load_2d(&map_b, &full[stage], sb + stage * B_BYTES, kb * BK, tn * BN);
+          tma_load_2d(&map_a, &full[stage], sa + stage * A_BYTES, kb * BKE, tm * BM);
+          tma_load_2d(&map_b, &full[stage], sb + stage * B_BYTES, kb * BKE, tn * BN);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(BM, BN);
+      constexpr uint32_t idesc = TF32 ? make_idesc_tf32(BM, BN) : make_idesc(BM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -248,7 +269,10 @@ k_gemm_bf16(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           for (int k = 0; k < BK / UMMA_K; ++k) {
             const uint64_t ad = smem_desc_sw128(a0 + k * UMMA_K * 2);
             const uint64_t bd = smem_desc_sw128(b0 + k * UMMA_K * 2);
-            tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (TF32)
+              tc_mma_tf32(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            else
+              tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
           tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -976,8 +1000,72 @@ int make_map(const Driver* d, CUtensorMap* map, const void* base, long long rows
   return PM_OK;
 }
 
+int make_map_f32(const Driver* d, CUtensorMap* map, const void* base, long long rows,
+                 long long cols, long long ld, int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = d->tensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                       const_cast<void*>(base), dims, strides, box, estr,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled(f32) failed: CUresult %d", (int)r);
+    return PM_ERR_CUDA;
+  }
+  return PM_OK;
+}
+
 }  // namespace gemm
 }  // namespace pm
+
+extern "C" int pm_gemm_tf32(const float* A, int64_t lda, const float* Bt, int64_t ldb, float* C,
+                            int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t accumulate,
+                            void* stream) {
+  using namespace pm::gemm;
+  if (!A || !Bt || !C || M <= 0 || N <= 0 || K <= 0 || lda < K || ldb < K || ldc < N)
+    return pm::set_error("pm_gemm_tf32: bad arguments"), PM_ERR_INVALID;
+  if ((lda % 4) || (ldb % 4) || ((uintptr_t)A % 16) || ((uintptr_t)Bt % 16))
+    return pm::set_error("pm_gemm_tf32: A/Bt need 16-byte aligned rows (ld % 4 == 0)"),
+           PM_ERR_UNSUPPORTED;
+  if (M > (1LL << 31) || N > (1LL << 31) || K > (1LL << 31))
+    return pm::set_error("pm_gemm_tf32: dimension too large"), PM_ERR_UNSUPPORTED;
+  const pm::Driver* d = pm::driver();
+  if (!d) return PM_ERR_CUDA;
+  CUtensorMap ma, mb;
+  int rc = make_map_f32(d, &ma, A, M, K, lda, BM);
+  if (rc) return rc;
+  rc = make_map_f32(d, &mb, Bt, N, K, ldb, BN);
+  if (rc) return rc;
+  Params p{};
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  p.tiles_m = (int)((M + BM - 1) / BM);
+  p.tiles_n = (int)((N + BN - 1) / BN);
+  p.k_blocks = (int)((K + 31) / 32);
+  p.c32 = C;
+  p.ldc = ldc;
+  p.accumulate = accumulate != 0;
+  p.group_m = 8;
+  static bool attr_done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return pm::set_error("pm_gemm_tf32: device id"), PM_ERR_UNSUPPORTED;
+  if (!attr_done[dev]) {
+    PM_CUDA_TRY(cudaFuncSetAttribute(k_gemm_1sm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SMEM_BYTES));
+    attr_done[dev] = true;
+  }
+  const long long ntiles = (long long)p.tiles_m * p.tiles_n;
+  int grid = pm::num_sms();
+  if (ntiles < grid) grid = (int)ntiles;
+  k_gemm_1sm<true><<<grid, kThreads, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, p);
+  PM_CUDA_TRY(cudaGetLastError());
+  return PM_OK;
+}
 
 extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t ldb, void* C,
                             int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t c_bf16,
@@ -1030,7 +1118,9 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return pm::set_error("pm_gemm_bf16: device id"), PM_ERR_UNSUPPORTED;
   if (!attr_done[dev]) {
-    PM_CUDA_TRY(cudaFuncSetAttribute(k_gemm_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PM_CUDA_TRY(cudaFuncSetAttribute(k_gemm_1sm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SMEM_BYTES));
+    PM_CUDA_TRY(cudaFuncSetAttribute(k_gemm_1sm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      SMEM_BYTES));
     PM_CUDA_TRY(cudaFuncSetAttribute(two::k_gemm_bf16_2sm,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, two::SMEM2));
@@ -1107,7 +1197,7 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
   const long long ntiles = (long long)p.tiles_m * p.tiles_n;
   int grid = pm::num_sms();
   if (ntiles < grid) grid = (int)ntiles;
-  k_gemm_bf16<<<grid, kThreads, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, p);
+  k_gemm_1sm<false><<<grid, kThreads, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, p);
   PM_CUDA_TRY(cudaGetLastError());
   return PM_OK;
 }

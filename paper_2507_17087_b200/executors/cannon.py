@@ -1,0 +1,204 @@
+"""Mapped Cannon (BASELINE configs[0]) and Solomonik 2.5D (configs[2]).
+
+Grid q x q x c (c = 1: Cannon; c > 1: 2.5D with c replication layers).  The
+tile launch is mapped onto the GPUs by a Mapple hierarchical block mapper --
+nodes block the tile grid, the processors of a node cycle over it (the paper's
+Fig-12 `cannon_mm` / `solomonik_mm` mappers) -- evaluated by
+the K1 kernel; the mapping must be a bijection onto the GPUs.
+
+GPU (i, j, l) starts with the 2-D blocks A(i, j) and B(i, j) (replicated on
+every layer).  Layer l runs Cannon steps t in [l q/c, (l+1) q/c): it first
+skews (A(i, (i+j+t0) mod q) and B((i+j+t0) mod q, j) are pulled from their
+holders), then alternates C += A*B with the Cannon shifts (A from the right
+neighbour, B from the neighbour below), each a copy-engine pull of the
+neighbour's current block over NVLink; a stream-ordered 4-byte NCCL
+all-reduce per round orders the shifts (no data goes through NCCL).  With
+c > 1 every step's product is reduce-added straight into the layer that owns
+those rows of C (TMA `.add` over NVLink), i.e. the 2.5D reduction is fused into
+the GEMMs.  fp32 operands run on the TF32 tensor cores, bf16 on the bf16 path.
+"""
+
+from __future__ import annotations
+
+from math import isqrt
+
+from .. import native
+from ..dsl import compile_mapper, parse
+from ..spaces import MachineShape
+from .summa import synth
+
+HIER_MAPPERS = """
+m = Machine(GPU)
+def tiles2d(Tuple ipoint, Tuple ispace):
+    mn = m.decompose(0, ispace)
+    mp = mn.decompose(2, ispace / mn[:-1])
+    blk = tuple(ipoint[i] * mp.size[i] / ispace[i] for i in (0, 1))
+    cyc = tuple(ipoint[i] % mp.size[i + 2] for i in (0, 1))
+    return mp[*blk, *cyc]
+def tiles3d(Tuple ipoint, Tuple ispace):
+    mn = m.decompose(0, ispace)
+    mp = mn.decompose(3, ispace / mn[:-1])
+    blk = tuple(ipoint[i] * mp.size[i] / ispace[i] for i in (0, 1, 2))
+    cyc = tuple(ipoint[i] % mp.size[i + 3] for i in (0, 1, 2))
+    return mp[*blk, *cyc]
+IndexTaskMap cannon tiles2d
+IndexTaskMap solomonik tiles3d
+"""
+
+
+def cannon_moves(q: int, c: int = 1) -> int:
+    """Block moves of the schedule (skew + shifts), A and B, summed over GPUs."""
+    moves = 0
+    steps = q // c
+    for layer in range(c):
+        t0 = layer * steps
+        for i in range(q):
+            for j in range(q):
+                moves += (i + t0) % q != 0  # skew: A(i, i+j+t0) held by (i, i+j+t0)
+                moves += (j + t0) % q != 0  # skew: B(i+j+t0, j) held by (i+j+t0, j)
+        if q > 1:
+            moves += (steps - 1) * 2 * q * q  # every shift moves one A and one B per GPU
+    return moves
+
+
+def split(n, parts, i):
+    return (n * i // parts, n * (i + 1) // parts)
+
+
+class MappedCannon:
+    def __init__(self, N: int, *, layers: int = 1, rank: int = 0, world: int = 1, group=None,
+                 dtype: str = "fp32", machine=None, seed: int = 0):
+        torch = native.require_cuda()
+        import torch.distributed as dist
+
+        from ..peer import PeerBuffers
+
+        c = layers
+        q = isqrt(world // c)
+        if q * q * c != world or q % c:
+            raise ValueError(f"{world} GPUs do not form a q x q x c grid with c | q (c={c})")
+        if dtype == "fp32" and c > 1:
+            raise ValueError("the 2.5D layer reduction adds atomically over NVLink: use bf16")
+        self.q, self.c, self.N = q, c, N
+        self.rank, self.world, self.group = rank, world, group
+        self.dtype = dtype
+        tdt = torch.float32 if dtype == "fp32" else torch.bfloat16
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        # Mapple mapping of the tile launch (K1)
+        if machine is None:
+            machine = (2, world // 2) if (c == 1 and world % 2 == 0 and world > 2) else (world, 1)
+        prog = parse(HIER_MAPPERS)
+        if c == 1:
+            fn = compile_mapper(prog, "cannon", MachineShape("GPU", *machine))
+            owners = fn.map_ispace((q, q)).tolist()
+            coords = [(i, j, 0) for i in range(q) for j in range(q)]
+        else:
+            fn = compile_mapper(prog, "solomonik", MachineShape("GPU", *machine))
+            owners = fn.map_ispace((q, q, c)).tolist()
+            coords = [(i, j, l) for i in range(q) for j in range(q) for l in range(c)]
+        if sorted(owners) != list(range(world)):
+            raise ValueError("the tile mapping is not a bijection onto the GPUs")
+        self.machine = machine
+        self.owner = {xyz: r for xyz, r in zip(coords, owners)}
+        self.coord = next(k for k, v in self.owner.items() if v == rank)
+        i, j, l = self.coord
+        nb = N // q
+        if nb * q != N:
+            raise ValueError("N must be divisible by q")
+        self.nb = nb
+        # operand blocks: cur / next buffers for the shifts; Bt stored transposed
+        self.A = [torch.empty(nb, nb, dtype=tdt, device=self.device) for _ in range(2)]
+        self.Bt = [torch.empty(nb, nb, dtype=tdt, device=self.device) for _ in range(2)]
+        self.A0 = synth((i * nb, (i + 1) * nb), (j * nb, (j + 1) * nb), N, seed,
+                        self.device, dtype=tdt)
+        # Bt(j-cols, i-k) = B(i-block, j-block)^T
+        self.B0 = synth((j * nb, (j + 1) * nb), (i * nb, (i + 1) * nb), N, seed + 1,
+                        self.device, dtype=tdt)
+        # C rows owned by this layer (reduce-scatter target), double-buffered
+        self.my_rows = split(nb, c, l)
+        self.C = [torch.zeros(self.my_rows[1] - self.my_rows[0], nb, dtype=torch.float32,
+                              device=self.device) for _ in range(2)]
+        self.peers = PeerBuffers({"A0": self.A0, "B0": self.B0, "Acur0": self.A[0],
+                                  "Acur1": self.A[1], "Bcur0": self.Bt[0], "Bcur1": self.Bt[1],
+                                  "C0": self.C[0], "C1": self.C[1]}, rank, world, group)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._dist = dist if world > 1 else None
+        self.step_i = 0
+        self.moved_blocks = 0
+        esz = 4 if dtype == "fp32" else 2
+        self.block_bytes = nb * nb * esz
+        self.flops = 2 * nb * nb * nb * (q // c)
+        torch.cuda.synchronize()
+        if self._dist:
+            dist.barrier(group=group)
+
+    def _barrier(self):
+        if self._dist:
+            self._dist.all_reduce(self.flag, group=self.group)
+
+    def _pull(self, name, src_rank, dst_tensor, stream):
+        from ..peer import copy2d
+
+        pitch = self.nb * dst_tensor.element_size()
+        src = self.peers.ptrs[name][src_rank]
+        if src_rank == self.rank:
+            src = self.peers.ptrs[name][self.rank]
+        copy2d(dst_tensor.data_ptr(), pitch, src, pitch, pitch, self.nb, stream)
+
+    def step(self, stream=None):
+        """One full multiply (all Cannon / 2.5D steps and the layer reduction)."""
+        torch = native.require_cuda()
+        lib = native.lib()
+        cs = stream or torch.cuda.current_stream()
+        q, c = self.q, self.c
+        i, j, l = self.coord
+        buf = self.step_i % 2
+        self.step_i += 1
+        if c > 1:
+            self.C[1 - buf].zero_()
+        self._barrier()
+        steps = q // c
+        t0 = l * steps
+        k0 = (i + j + t0) % q
+        moved = 0
+        # skew: A(i, k0) from its holder (i, k0, l), B(k0, j) from (k0, j, l)
+        cur = 0
+        self._pull("A0", self.owner[(i, k0, l)], self.A[cur], cs)
+        self._pull("B0", self.owner[(k0, j, l)], self.Bt[cur], cs)
+        moved += (self.owner[(i, k0, l)] != self.rank) + (self.owner[(k0, j, l)] != self.rank)
+        self._barrier()
+        for s in range(steps):
+            # C(rows of layer d) += A(i,k) B(k,j); the last layer-local step order is fixed
+            for d in range(c):
+                r0, r1 = split(self.nb, c, d)
+                dst = self.owner[(i, j, d)]
+                cptr = self.peers.ptrs[f"C{buf}"][dst]
+                a = self.A[cur][r0:r1]
+                if self.dtype == "fp32":
+                    native.check(lib.pm_gemm_tf32(a.data_ptr(), self.nb, self.Bt[cur].data_ptr(),
+                                                  self.nb, cptr, self.nb, r1 - r0, self.nb,
+                                                  self.nb, int(s > 0 or c > 1),
+                                                  native.stream_ptr(cs)), "pm_gemm_tf32")
+                else:
+                    native.check(lib.pm_gemm_bf16(a.data_ptr(), self.nb, self.Bt[cur].data_ptr(),
+                                                  self.nb, cptr, self.nb, r1 - r0, self.nb,
+                                                  self.nb, 0, 2 if c > 1 else int(s > 0),
+                                                  native.stream_ptr(cs)), "pm_gemm_bf16")
+            if s + 1 < steps:  # Cannon shift: A from the right, B from below
+                nxt = 1 - cur
+                right = self.owner[(i, (j + 1) % q, l)]
+                below = self.owner[((i + 1) % q, j, l)]
+                self._pull(f"Acur{cur}", right, self.A[nxt], cs)
+                self._pull(f"Bcur{cur}", below, self.Bt[nxt], cs)
+                moved += (right != self.rank) + (below != self.rank)
+                self._barrier()
+                cur = nxt
+        self.moved_blocks = moved
+        return self.C[buf]
+
+    def result(self):
+        self._barrier()
+        return self.C[(self.step_i - 1) % 2]
+
+    def close(self):
+        self.peers.close()

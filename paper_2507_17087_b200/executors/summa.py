@@ -137,12 +137,18 @@ def tile_mapper(world: int, mapping: str):
     return compile_mapper(prog, f"gemm_{mapping}", MachineShape("GPU", world, 1))
 
 
-def synth(rows: tuple, cols: tuple, ld: int, seed: int, device):
-    """Deterministic U(-1, 1) bf16 block of a virtual [*, ld] matrix.
+def synth(rows: tuple, cols: tuple, ld: int, seed: int, device, dtype=None):
+    """Deterministic U(-1, 1) block (bf16 unless `dtype`) of a virtual [*, ld] matrix.
 
     Element (i, k) depends only on (i * ld + k, seed), so every rank can
     materialise exactly its own slice of the global operands.
     """
+    if dtype is not None:
+        return synth_f32(rows, cols, ld, seed, device).to(dtype)
+    return synth_f32(rows, cols, ld, seed, device).to(native.require_cuda().bfloat16)
+
+
+def synth_f32(rows: tuple, cols: tuple, ld: int, seed: int, device):
     torch = native.require_cuda()
     i = torch.arange(rows[0], rows[1], device=device, dtype=torch.int64).view(-1, 1)
     k = torch.arange(cols[0], cols[1], device=device, dtype=torch.int64).view(1, -1)
@@ -150,7 +156,7 @@ def synth(rows: tuple, cols: tuple, ld: int, seed: int, device):
     x = (x * 1103515245 + 12345 + seed * 7919) % (1 << 31)
     x = x ^ (x >> 13)
     x = (x * 69069 + 1) % (1 << 31)
-    return ((x.to(torch.float32) / float(1 << 30)) - 1.0).to(torch.bfloat16)
+    return (x.to(torch.float32) / float(1 << 30)) - 1.0
 
 
 @dataclass(frozen=True)

@@ -31,3 +31,26 @@ def tile_gemm(A, Bt, C=None, *, accumulate: bool = False, out_dtype=None, stream
             M, N, K, int(C.dtype == torch.bfloat16), int(accumulate),
             native.stream_ptr(stream)), "pm_gemm_bf16")
     return C
+
+
+def tile_gemm_tf32(A, Bt, C=None, *, accumulate: bool = False, stream=None):
+    """C (+)= A @ Bt.T on fp32 operands via the TF32 tensor cores (fp32 accumulate)."""
+    torch = native.require_cuda()
+    if A.dtype != torch.float32 or Bt.dtype != torch.float32:
+        raise ValueError("A and Bt must be fp32")
+    if A.dim() != 2 or Bt.dim() != 2 or A.shape[1] != Bt.shape[1]:
+        raise ValueError(f"shape mismatch: A {tuple(A.shape)}, Bt {tuple(Bt.shape)}")
+    if A.stride(1) != 1 or Bt.stride(1) != 1:
+        raise ValueError("A and Bt must be row-major (K contiguous)")
+    M, K = A.shape
+    N = Bt.shape[0]
+    if C is None:
+        C = (torch.zeros if accumulate else torch.empty)((M, N), dtype=torch.float32,
+                                                         device=A.device)
+    if C.shape != (M, N) or C.stride(1) != 1 or C.dtype != torch.float32:
+        raise ValueError("C must be a row-major fp32 [M, N] tensor")
+    with torch.cuda.device(A.device):
+        native.check(native.lib().pm_gemm_tf32(
+            A.data_ptr(), A.stride(0), Bt.data_ptr(), Bt.stride(0), C.data_ptr(), C.stride(0),
+            M, N, K, int(accumulate), native.stream_ptr(stream)), "pm_gemm_tf32")
+    return C

@@ -113,3 +113,5 @@ def stream_ptr(stream=None) -> int:
 
 
 SIGNATURES["pm_stencil_sweep"] = (ctypes.c_int, [ctypes.c_void_p, _I32, _VP])
+SIGNATURES["pm_gemm_tf32"] = (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64,
+                                             _I32, _VP])

@@ -60,3 +60,18 @@ def test_gemm_strided_views(cuda):
     Bt = big[100:356, 512:]    # ldb = 1024
     C = tile_gemm(A, Bt)
     assert _rel(C, _ref(A, Bt)) < 1e-4
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 512, 512), (1000, 700, 320), (128, 256, 32), (2048, 1024, 4096)])
+def test_tf32_gemm(cuda, M, N, K):
+    from paper_2507_17087_b200.gemm import tile_gemm_tf32
+
+    torch = cuda
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.rand(M, K, device="cuda", generator=g) * 2 - 1
+    Bt = torch.rand(N, K, device="cuda", generator=g) * 2 - 1
+    C = tile_gemm_tf32(A, Bt)
+    R = A.double() @ Bt.double().T
+    assert _rel(C, R) <= TOL  # tf32 operands: ~1e-3 relative
+    C2 = tile_gemm_tf32(A, Bt, C.clone(), accumulate=True)
+    assert _rel(C2, 2 * R) <= TOL

@@ -51,3 +51,11 @@ def test_peer_gemm_reduce_add():
         pytest.skip("needs 2 GPUs")
     v = _run("dist_peer_gemm_check.py", 2, 29720)
     assert v["ok"], v
+
+
+@pytest.mark.parametrize("n", [1, 4, 8])
+def test_cannon(n):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    v = _run("dist_cannon_check.py", n, 29730 + n)
+    assert v["ok"], v
