@@ -65,6 +65,35 @@ def split(n, parts, i):
     return (n * i // parts, n * (i + 1) // parts)
 
 
+def cannon_schedule(q: int, c: int, coord):
+    """The per-GPU op list of one multiply, shared by the executor and the CPU
+    schedule test.  Ops:
+      ("pull", src_buffer, src_coord, dst_slot)  -- copy a peer's block into A/B slot
+      ("barrier",)                               -- stream-ordered all-GPU barrier
+      ("gemm", slot, dst_layer)                  -- C(rows of dst_layer) += A[slot] B[slot]
+    src_buffer names "A0"/"B0" (the initial blocks) or "Acur<s>"/"Bcur<s>"
+    (a peer's current operand in slot s); dst_slot is (kind, slot)."""
+    i, j, l = coord
+    steps = q // c
+    t0 = l * steps
+    k0 = (i + j + t0) % q
+    ops = [("barrier",),
+           ("pull", "A0", (i, k0, l), ("A", 0)),
+           ("pull", "B0", (k0, j, l), ("B", 0)),
+           ("barrier",)]
+    cur = 0
+    for s in range(steps):
+        for d in range(c):
+            ops.append(("gemm", cur, d))
+        if s + 1 < steps:  # Cannon shift: A from the right, B from below
+            nxt = 1 - cur
+            ops.append(("pull", f"Acur{cur}", (i, (j + 1) % q, l), ("A", nxt)))
+            ops.append(("pull", f"Bcur{cur}", ((i + 1) % q, j, l), ("B", nxt)))
+            ops.append(("barrier",))
+            cur = nxt
+    return ops
+
+
 class MappedCannon:
     def __init__(self, N: int, *, layers: int = 1, rank: int = 0, world: int = 1, group=None,
                  dtype: str = "fp32", machine=None, seed: int = 0):
@@ -156,43 +185,33 @@ class MappedCannon:
         self.step_i += 1
         if c > 1:
             self.C[1 - buf].zero_()
-        self._barrier()
-        steps = q // c
-        t0 = l * steps
-        k0 = (i + j + t0) % q
         moved = 0
-        # skew: A(i, k0) from its holder (i, k0, l), B(k0, j) from (k0, j, l)
-        cur = 0
-        self._pull("A0", self.owner[(i, k0, l)], self.A[cur], cs)
-        self._pull("B0", self.owner[(k0, j, l)], self.Bt[cur], cs)
-        moved += (self.owner[(i, k0, l)] != self.rank) + (self.owner[(k0, j, l)] != self.rank)
-        self._barrier()
-        for s in range(steps):
-            # C(rows of layer d) += A(i,k) B(k,j); the last layer-local step order is fixed
-            for d in range(c):
-                r0, r1 = split(self.nb, c, d)
-                dst = self.owner[(i, j, d)]
-                cptr = self.peers.ptrs[f"C{buf}"][dst]
-                a = self.A[cur][r0:r1]
-                if self.dtype == "fp32":
-                    native.check(lib.pm_gemm_tf32(a.data_ptr(), self.nb, self.Bt[cur].data_ptr(),
-                                                  self.nb, cptr, self.nb, r1 - r0, self.nb,
-                                                  self.nb, int(s > 0 or c > 1),
-                                                  native.stream_ptr(cs)), "pm_gemm_tf32")
-                else:
-                    native.check(lib.pm_gemm_bf16(a.data_ptr(), self.nb, self.Bt[cur].data_ptr(),
-                                                  self.nb, cptr, self.nb, r1 - r0, self.nb,
-                                                  self.nb, 0, 2 if c > 1 else int(s > 0),
-                                                  native.stream_ptr(cs)), "pm_gemm_bf16")
-            if s + 1 < steps:  # Cannon shift: A from the right, B from below
-                nxt = 1 - cur
-                right = self.owner[(i, (j + 1) % q, l)]
-                below = self.owner[((i + 1) % q, j, l)]
-                self._pull(f"Acur{cur}", right, self.A[nxt], cs)
-                self._pull(f"Bcur{cur}", below, self.Bt[nxt], cs)
-                moved += (right != self.rank) + (below != self.rank)
+        first = True  # the first local product overwrites C (Cannon); 2.5D always adds
+        for op in cannon_schedule(q, c, self.coord):
+            if op[0] == "barrier":
                 self._barrier()
-                cur = nxt
+            elif op[0] == "pull":
+                _, name, src, (kind, slot) = op
+                dst = self.A[slot] if kind == "A" else self.Bt[slot]
+                self._pull(name, self.owner[src], dst, cs)
+                moved += self.owner[src] != self.rank
+            else:  # C(rows of layer d) += A(i,k) B(k,j), reduce-added into the owning layer
+                _, slot, d = op
+                r0, r1 = split(self.nb, c, d)
+                cptr = self.peers.ptrs[f"C{buf}"][self.owner[(i, j, d)]]
+                a = self.A[slot][r0:r1]
+                acc = 2 if c > 1 else int(not first)
+                if self.dtype == "fp32":
+                    native.check(lib.pm_gemm_tf32(a.data_ptr(), self.nb, self.Bt[slot].data_ptr(),
+                                                  self.nb, cptr, self.nb, r1 - r0, self.nb,
+                                                  self.nb, acc, native.stream_ptr(cs)),
+                                 "pm_gemm_tf32")
+                else:
+                    native.check(lib.pm_gemm_bf16(a.data_ptr(), self.nb, self.Bt[slot].data_ptr(),
+                                                  self.nb, cptr, self.nb, r1 - r0, self.nb,
+                                                  self.nb, 0, acc, native.stream_ptr(cs)),
+                                 "pm_gemm_bf16")
+                first = False
         self.moved_blocks = moved
         return self.C[buf]
 
