@@ -112,6 +112,29 @@ void pm_plan_destroy(pm_plan* plan);
 int pm_map_batch(const pm_plan* plan, const int32_t* points, int64_t n, int64_t first,
                  int32_t* out_proc, uint64_t* status, void* stream);
 
+/* Fused map + partition (K1 + K2 without materialising the processor ids)
+ *   <- cmd_map's loop (cli.py:149-170) feeding expand_shards / shard_policy
+ *      (tasksim/sim.py:67-120): the stable partition of launch points
+ *      [first, first + n) by processor id, ids in [0, nbins), nbins <= 64.
+ * Pass 1, pm_map_hist: counts[b], offsets[b] (exclusive prefix) per processor;
+ *   the per-tile histogram stays in `scratch` for pass 2.
+ * Pass 2, pm_map_scatter: with the same n / first / nbins / scratch, writes
+ *   point index (index_base + i) at its stable slot: perm[offsets[b] + r] or,
+ *   when bin_dst != NULL, ((int32_t*)bin_dst[2 b])[offsets[b] + r + bin_dst[2 b + 1]]
+ *   (bin_dst: device array of nbins (pointer, element shift) pairs; the pointers
+ *   may be peer-GPU memory).  out_proc (nullable) receives the processor ids.
+ * Failures: as pm_map_batch (status, caller-initialised to UINT64_MAX); a
+ *   failing point is left out of the partition.  Explicit mode: `points` as in
+ *   pm_map_batch, indexed by i.  scratch: pm_map_partition_scratch_bytes(). */
+size_t pm_map_partition_scratch_bytes(int64_t n, int32_t nbins);
+int pm_compile_check_fused(const pm_program* prog);
+int pm_map_hist(pm_plan* plan, const int32_t* points, int64_t n, int64_t first, int32_t nbins,
+                int64_t* counts, int64_t* offsets, uint64_t* status, void* scratch,
+                size_t scratch_bytes, void* stream);
+int pm_map_scatter(pm_plan* plan, const int32_t* points, int64_t n, int64_t first, int32_t nbins,
+                   int32_t* out_proc, int32_t* perm, const int64_t* bin_dst, int64_t index_base,
+                   uint64_t* status, void* scratch, size_t scratch_bytes, void* stream);
+
 /* Stable partition of n processor ids in [0, nbins):
  *   counts[b]  = #points with id b                    (int64, device)
  *   offsets[b] = exclusive prefix of counts           (int64, device)

@@ -29,6 +29,9 @@ struct HaloKey {
   int halo[3];
   int rank;
   int nprocs;
+  static constexpr bool kVec4 = false;
+  static constexpr bool kPeek = false;
+  __device__ __forceinline__ void uniform(long long, int, int) const {}
   __device__ __forceinline__ int operator()(long long i) const {
     const int slots = 2 * rank;
     const long long cell = i / slots;
@@ -54,7 +57,10 @@ struct HaloSink {
   long long* __restrict__ cells;
   signed char* __restrict__ dims;
   int slots;
-  __device__ __forceinline__ void put(long long pos, long long i) const {
+  __device__ __forceinline__ void put_run(int b, long long pos, long long i, int count) const {
+    for (int k = threadIdx.x; k < count; k += blockDim.x) put(b, pos + k, i + k);
+  }
+  __device__ __forceinline__ void put(int, long long pos, long long i) const {
     const long long c = i / slots;
     cells[pos] = c;
     if (dims) dims[pos] = (signed char)(i - c * slots);

@@ -24,6 +24,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "plan.h"
 #include "pm_common.h"
 
 namespace pm {
@@ -286,21 +287,114 @@ pm_map_points(const int* __restrict__ pts, long long n, long long first,
   }
 };
 
+// Fused map + partition kernels: the key of a point is its processor id,
+// computed in registers by pm_eval -- the id array of K1 is never read back.
+const char* kFused = R"CUDA(
+#include "partition_device.cuh"
+
+struct PmMapKey {
+  const int* pts;
+  long long first;
+  unsigned long long* status;
+  int* out;  // optional processor-id output (scatter pass)
+  int nbins;
+  static constexpr bool kVec4 = false;
+  static constexpr bool kPeek = true;
+  __device__ __forceinline__ int peek(long long i) const {
+    int site = 0;
+    return pm_eval(first + i, pts + i * PM_K, &site);
+  }
+  __device__ __forceinline__ void uniform(long long base, int count, int b) const {
+    if (out)
+      for (int k = threadIdx.x; k < count; k += blockDim.x) out[base + k] = b;
+  }
+  __device__ __forceinline__ int operator()(long long i) const {
+    int site = 0;
+    int r = pm_eval(first + i, pts + i * PM_K, &site);
+    if (r >= nbins) { site = 0xFFFE; r = -1; }
+    if (r < 0) pm_report(status, first + i, site);
+    if (out) out[i] = r;
+    return r;
+  }
+};
+
+struct PmPermSink {
+  int* __restrict__ perm;
+  long long base;
+  __device__ __forceinline__ void put(int, long long pos, long long i) const {
+    perm[pos] = (int)(base + i);
+  }
+  __device__ __forceinline__ void put_run(int, long long pos, long long i, int count) const {
+    pmdev::store_iota(perm + pos, (int)(base + i), count);
+  }
+};
+
+// per-bin destination: tab[2 b] = int32 pointer (possibly a peer GPU's), tab[2 b + 1] =
+// element shift applied to the local grouped position
+struct PmPeerSink {
+  const long long* __restrict__ tab;
+  long long base;
+  __device__ __forceinline__ void put(int b, long long pos, long long i) const {
+    int* p = reinterpret_cast<int*>(__ldg(tab + 2 * b));
+    p[pos + __ldg(tab + 2 * b + 1)] = (int)(base + i);
+  }
+  __device__ __forceinline__ void put_run(int b, long long pos, long long i, int count) const {
+    int* p = reinterpret_cast<int*>(__ldg(tab + 2 * b));
+    pmdev::store_iota(p + pos + __ldg(tab + 2 * b + 1), (int)(base + i), count);
+  }
+};
+
+extern "C" __global__ void __launch_bounds__(256)
+pm_map_hist(const int* pts, long long n, long long first, int nbins, long long ntiles,
+            long long* __restrict__ hist, unsigned long long* status) {
+  extern __shared__ __align__(16) int smem_words[];
+  const PmMapKey key{pts, first, status, nullptr, nbins};
+  pmdev::small_hist_body(key, n, nbins, ntiles, hist, smem_words);
+}
+
+extern "C" __global__ void __launch_bounds__(256)
+pm_map_scatter(const int* pts, long long n, long long first, int nbins, long long ntiles,
+               const long long* __restrict__ pos0, unsigned long long* status, int* out,
+               int* perm, long long base) {
+  extern __shared__ __align__(16) int smem_words[];
+  const PmMapKey key{pts, first, status, out, nbins};
+  pmdev::small_scatter_body(key, PmPermSink{perm, base}, n, nbins, ntiles, pos0, smem_words);
+}
+
+extern "C" __global__ void __launch_bounds__(256)
+pm_map_scatter_peer(const int* pts, long long n, long long first, int nbins, long long ntiles,
+                    const long long* __restrict__ pos0, unsigned long long* status, int* out,
+                    const long long* tab, long long base) {
+  extern __shared__ __align__(16) int smem_words[];
+  const PmMapKey key{pts, first, status, out, nbins};
+  pmdev::small_scatter_body(key, PmPeerSink{tab, base}, n, nbins, ntiles, pos0, smem_words);
+}
+)CUDA";
+
 std::mutex g_cache_mu;
 std::unordered_map<std::string, std::vector<char>> g_cubins;
 
-int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
+// Device half of the small-bin stable partition (partition_device.cuh), as text
+// for NVRTC; build/partition_device_src.inc is generated by the Makefile.
+const char kPartitionDevice[] =
+#include "partition_device_src.inc"
+    ;
+
+int nvrtc_compile(const std::string& src, std::vector<char>* cubin, bool with_partition = false) {
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    auto it = g_cubins.find(src);
+    auto it = g_cubins.find(with_partition ? "P" + src : src);
     if (it != g_cubins.end()) {
       *cubin = it->second;
       return PM_OK;
     }
   }
   nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, src.c_str(), "pm_point_program.cu", 0, nullptr, nullptr) !=
-      NVRTC_SUCCESS)
+  const char* hdr_src[] = {kPartitionDevice};
+  const char* hdr_name[] = {"partition_device.cuh"};
+  if (nvrtcCreateProgram(&prog, src.c_str(), "pm_point_program.cu", with_partition ? 1 : 0,
+                         with_partition ? hdr_src : nullptr,
+                         with_partition ? hdr_name : nullptr) != NVRTC_SUCCESS)
     return set_error("nvrtcCreateProgram failed"), PM_ERR_NVRTC;
   const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-device-int128", "-lineinfo",
                         "-default-device", "-w"};
@@ -319,8 +413,14 @@ int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
   cubin->resize(n);
   nvrtcGetCUBIN(prog, cubin->data());
   nvrtcDestroyProgram(&prog);
+  if (const char* dump = getenv("PM_DUMP_CUBIN")) {  // debugging: inspect with cuobjdump
+    if (FILE* f = fopen(dump, "wb")) {
+      fwrite(cubin->data(), 1, cubin->size(), f);
+      fclose(f);
+    }
+  }
   std::lock_guard<std::mutex> lk(g_cache_mu);
-  g_cubins.emplace(src, *cubin);
+  g_cubins.emplace(with_partition ? "P" + src : src, *cubin);
   return PM_OK;
 }
 
@@ -339,15 +439,23 @@ int generate(const pm_program* prog, std::string* out) {
 
 }  // namespace
 
-}  // namespace pm
+int plan_fused(pm_plan* p) {
+  std::lock_guard<std::mutex> lk(p->fused_mu);
+  if (p->fused_ready) return PM_OK;
+  std::vector<char> cubin;
+  int rc = nvrtc_compile(p->src + kFused, &cubin, true);
+  if (rc) return rc;
+  const Driver* d = driver();
+  if (!d) return PM_ERR_CUDA;
+  PM_CU_TRY(d->moduleLoadData(&p->fused_mod, cubin.data()));
+  PM_CU_TRY(d->moduleGetFunction(&p->fn_hist, p->fused_mod, "pm_map_hist"));
+  PM_CU_TRY(d->moduleGetFunction(&p->fn_scatter, p->fused_mod, "pm_map_scatter"));
+  PM_CU_TRY(d->moduleGetFunction(&p->fn_scatter_peer, p->fused_mod, "pm_map_scatter_peer"));
+  p->fused_ready = true;
+  return PM_OK;
+}
 
-struct pm_plan {
-  CUmodule mod = nullptr;
-  CUfunction fn = nullptr;
-  int n_coords = 0;
-  int implicit = 0;
-  int device = 0;
-};
+}  // namespace pm
 
 extern "C" {
 
@@ -370,6 +478,14 @@ int pm_compile_check(const pm_program* prog) {
   if (rc) return rc;
   std::vector<char> cubin;
   return pm::nvrtc_compile(src, &cubin);
+}
+
+int pm_compile_check_fused(const pm_program* prog) {
+  std::string src;
+  int rc = pm::generate(prog, &src);
+  if (rc) return rc;
+  std::vector<char> cubin;
+  return pm::nvrtc_compile(src + pm::kFused, &cubin, true);
 }
 
 int pm_plan_create(const pm_program* prog, pm_plan** out) {
@@ -401,6 +517,7 @@ int pm_plan_create(const pm_program* prog, pm_plan** out) {
   }
   p->n_coords = prog->n_coords;
   p->implicit = prog->implicit;
+  p->src = src;
   *out = p;
   return PM_OK;
 }
@@ -409,6 +526,7 @@ void pm_plan_destroy(pm_plan* plan) {
   if (!plan) return;
   const pm::Driver* d = pm::driver();
   if (d && plan->mod) d->moduleUnload(plan->mod);
+  if (d && plan->fused_mod) d->moduleUnload(plan->fused_mod);
   delete plan;
 }
 

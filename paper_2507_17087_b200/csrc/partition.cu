@@ -22,6 +22,9 @@ struct ProcKey {
   int nbins;
   unsigned long long* bad;
   bool vec_ok;  // proc is 16-byte aligned: keys4() may use vector loads
+  static constexpr bool kVec4 = true;
+  static constexpr bool kPeek = false;
+  __device__ __forceinline__ void uniform(long long, int, int) const {}
   __device__ __forceinline__ int check(int b, long long i) const {
     if (b < 0 || b >= nbins) {
       atomicMin(bad, (unsigned long long)i);
@@ -40,7 +43,10 @@ struct ProcKey {
 
 struct PermSink {
   int* __restrict__ perm;
-  __device__ __forceinline__ void put(long long pos, long long i) const { perm[pos] = (int)i; }
+  __device__ __forceinline__ void put(int, long long pos, long long i) const { perm[pos] = (int)i; }
+  __device__ __forceinline__ void put_run(int, long long pos, long long i, int count) const {
+    pmdev::store_iota(perm + pos, (int)i, count);
+  }
 };
 
 // `bad` is an unsigned atomicMin target that starts at UINT64_MAX; report

@@ -1,0 +1,275 @@
+// Device half of the small-bin stable counting partition (<= 64 bins).
+//
+// Self-contained (no includes, no host code) so the same text is compiled
+// twice: statically by nvcc for K2 / K3 (stable_partition.cuh) and, embedded
+// as a string, by NVRTC next to a generated mapping program for the fused
+// map + partition kernels (mapping.cpp) -- there the key of a point is its
+// processor id computed in registers, so no id array is ever read.
+//
+// Key concept:  int operator()(long long i)  -> bin of item i, or -1 (no output)
+//               static constexpr bool kVec4; if true also
+//               bool vec_ok; int keys4(long long i) -> 4 int8 bins of items i..i+3
+//               void uniform(long long base, int count, int bin): the scatter
+//               skipped evaluating items [base, base + count), all in `bin`
+//               static constexpr bool kPeek; if true also int peek(long long i):
+//               the bin without side effects or checks (histogram fast path)
+// Sink concept: void put(int bin, long long pos, long long i)
+//               void put_run(int bin, long long pos, long long i, int count): the
+//               whole CTA stores items i .. i + count - 1 at pos .. pos + count - 1
+//
+// Thread t of a 4096-item tile owns the contiguous items [16 t, 16 t + 16);
+// counts live in lane-private shared cells cnt[bin][thread] (bank = thread %
+// 32: no conflicts, no atomics).  The scatter scans cnt along the threads of
+// every bin and each thread writes its items at base + prefix + running count.
+#pragma once
+
+namespace pmdev {
+
+constexpr int kPartThreads = 256;
+constexpr int kPartWarps = kPartThreads / 32;
+constexpr int kSmallBins = 64;
+constexpr int kIPT = 16;                          // items per thread
+constexpr int kSmallTile = kPartThreads * kIPT;   // 4096 items per tile
+
+// dst[k] = v0 + k for k < count, by the whole CTA: 16-byte streaming stores
+// between a scalar head (to 16-byte alignment) and tail.
+__device__ __forceinline__ void store_iota(int* dst, int v0, int count) {
+  int head = (int)((4 - (((unsigned long long)dst >> 2) & 3)) & 3);
+  if (head > count) head = count;
+  if ((int)threadIdx.x < head) dst[threadIdx.x] = v0 + (int)threadIdx.x;
+  const int nvec = (count - head) >> 2;
+  int4* body = reinterpret_cast<int4*>(dst + head);
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const int e = v0 + head + 4 * v;
+    asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(body + v), "r"(e),
+                 "r"(e + 1), "r"(e + 2), "r"(e + 3) : "memory");
+  }
+  for (int k = head + 4 * nvec + threadIdx.x; k < count; k += blockDim.x) dst[k] = v0 + k;
+}
+
+// Phase A of both passes: keys evaluated in coalesced order (item base + t +
+// 256 m), stored as int8 bins in shared memory.
+template <class Key>
+__device__ __forceinline__ void small_keys(const Key& key, long long base, long long n,
+                                           signed char* __restrict__ sbin) {
+  if constexpr (Key::kVec4) {
+    // 4 consecutive keys per 16-byte load (e.g. processor ids in HBM)
+#pragma unroll
+    for (int m = 0; m < kIPT / 4; ++m) {
+      const int off = (m * kPartThreads + threadIdx.x) * 4;
+      const long long i = base + off;
+      int packed;
+      if (i + 3 < n && key.vec_ok) {
+        packed = key.keys4(i);
+      } else {
+        packed = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          packed |= ((i + q < n ? key(i + q) : -1) & 0xFF) << (8 * q);
+      }
+      *reinterpret_cast<int*>(sbin + off) = packed;
+    }
+  } else {
+#pragma unroll 4
+    for (int m = 0; m < kIPT; ++m) {
+      const int off = m * kPartThreads + threadIdx.x;
+      const long long i = base + off;
+      sbin[off] = (signed char)(i < n ? key(i) : -1);
+    }
+  }
+}
+
+// Histogram pass: order is irrelevant, so every thread run-length counts the
+// keys it evaluates (coalesced order) and flushes a run into its warp's
+// shared histogram with one atomic when the bin changes -- block mappings
+// flush once per thread.  shared: h[kPartWarps][nbins]
+template <class Key>
+__device__ __forceinline__ void small_hist_body(const Key& key, long long n, int nbins,
+                                                long long ntiles, long long* __restrict__ hist,
+                                                int* smem_words) {
+  int* h = smem_words;
+  for (int b = threadIdx.x; b < kPartWarps * nbins; b += kPartThreads) h[b] = 0;
+  __syncthreads();
+  const long long base = (long long)blockIdx.x * kSmallTile;
+  int* hw = h + (threadIdx.x >> 5) * nbins;
+  int run_bin = -1, run = 0;
+  auto add = [&](int b) {
+    if (b != run_bin) {
+      if (run_bin >= 0) atomicAdd(hw + run_bin, run);
+      run_bin = b;
+      run = 0;
+    }
+    ++run;
+  };
+  if constexpr (Key::kVec4) {
+#pragma unroll
+    for (int m = 0; m < kIPT / 4; ++m) {
+      const long long i = base + (long long)(m * kPartThreads + threadIdx.x) * 4;
+      if (i + 3 < n && key.vec_ok) {
+        const int packed = key.keys4(i);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) add((int)(signed char)(packed >> (8 * q)));
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) add(i + q < n ? key(i + q) : -1);
+      }
+    }
+  } else if (base + kSmallTile <= n) {  // full tile: no bounds checks
+    if constexpr (Key::kPeek) {
+      // unchecked evaluation; a failing / out-of-range item (bin outside
+      // [0, nbins)) is only flagged here and re-evaluated with reporting below
+      bool bad = false;
+#pragma unroll 4
+      for (int m = 0; m < kIPT; ++m) {
+        const int r = key.peek(base + m * kPartThreads + threadIdx.x);
+        const bool ok = (unsigned)r < (unsigned)nbins;
+        bad |= !ok;
+        add(ok ? r : -1);
+      }
+      if (bad)
+        for (int m = 0; m < kIPT; ++m) (void)key(base + m * kPartThreads + threadIdx.x);
+    } else {
+#pragma unroll 4
+      for (int m = 0; m < kIPT; ++m) add(key(base + m * kPartThreads + threadIdx.x));
+    }
+  } else {
+#pragma unroll 4
+    for (int m = 0; m < kIPT; ++m) {
+      const long long i = base + m * kPartThreads + threadIdx.x;
+      add(i < n ? key(i) : -1);
+    }
+  }
+  if (run_bin >= 0) atomicAdd(hw + run_bin, run);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += kPartThreads) {
+    int sum = 0;
+#pragma unroll
+    for (int w = 0; w < kPartWarps; ++w) sum += h[w * nbins + b];
+    hist[(long long)b * ntiles + blockIdx.x] = sum;
+  }
+}
+
+// shared: int8 bins[4096] | int16 stage[4096] | cnt[nbins][256] | start[nbins + 1]
+// pos0[b * ntiles + t] = first output slot of (bin b, tile t) (scanned histogram)
+template <class Key, class Sink>
+__device__ __forceinline__ void small_scatter_body(const Key& key, const Sink& sink, long long n,
+                                                   int nbins, long long ntiles,
+                                                   const long long* __restrict__ pos0,
+                                                   int* smem_words) {
+  signed char* sbin = reinterpret_cast<signed char*>(smem_words);
+  short* stage = reinterpret_cast<short*>(sbin + kSmallTile);
+  int* cnt = reinterpret_cast<int*>(stage + kSmallTile);
+  int* start = cnt + nbins * kPartThreads;
+  const long long base = (long long)blockIdx.x * kSmallTile;
+  // a full tile whose 4096 items all share one bin (the histogram says so:
+  // block mappings, the common case) is a straight copy of consecutive
+  // indices -- no key is evaluated or read at all
+  __shared__ int s_only;
+  if (threadIdx.x == 0) s_only = -1;
+  __syncthreads();
+  if (blockIdx.x + 1 < ntiles && threadIdx.x < nbins) {
+    const long long q = (long long)threadIdx.x * ntiles + blockIdx.x;
+    if (pos0[q + 1] - pos0[q] == kSmallTile) s_only = threadIdx.x;
+  }
+  __syncthreads();
+  if (s_only >= 0) {
+    const int only = s_only;
+    const long long p0 = pos0[(long long)only * ntiles + blockIdx.x];
+    key.uniform(base, kSmallTile, only);
+    sink.put_run(only, p0, base, kSmallTile);
+    return;
+  }
+  for (int b = 0; b < nbins; ++b) cnt[b * kPartThreads + threadIdx.x] = 0;
+  small_keys(key, base, n, sbin);
+  __syncthreads();
+  const int4 w = reinterpret_cast<const int4*>(sbin)[threadIdx.x];
+  const signed char* bb = reinterpret_cast<const signed char*>(&w);
+  int bins[kIPT];
+#pragma unroll
+  for (int j = 0; j < kIPT; ++j) bins[j] = bb[j];
+  int run_bin = -1, run = 0;
+#pragma unroll
+  for (int j = 0; j < kIPT; ++j) {
+    if (bins[j] != run_bin) {
+      if (run_bin >= 0) cnt[run_bin * kPartThreads + threadIdx.x] += run;
+      run_bin = bins[j];
+      run = 0;
+    }
+    ++run;
+  }
+  if (run_bin >= 0) cnt[run_bin * kPartThreads + threadIdx.x] += run;
+  __syncthreads();
+  // exclusive scan of each bin's row along the threads; row totals -> start[]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int b = warp; b < nbins; b += kPartWarps) {
+    int* row = cnt + b * kPartThreads;
+    int v[kPartThreads / 32];
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < kPartThreads / 32; ++k) {
+      v[k] = row[lane * (kPartThreads / 32) + k];
+      s += v[k];
+    }
+    int incl = s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += u;
+    }
+    int run_pre = incl - s;
+#pragma unroll
+    for (int k = 0; k < kPartThreads / 32; ++k) {
+      row[lane * (kPartThreads / 32) + k] = run_pre;
+      run_pre += v[k];
+    }
+    if (lane == 31) start[b] = incl;  // bin total in this tile
+  }
+  __syncthreads();
+  if (warp == 0) {  // start[b] = exclusive prefix of the bin totals (nbins <= 64)
+    const int t0 = lane < nbins ? start[lane] : 0;
+    const int t1 = lane + 32 < nbins ? start[lane + 32] : 0;
+    int a = t0, c = t1;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int ua = __shfl_up_sync(0xffffffffu, a, d), uc = __shfl_up_sync(0xffffffffu, c, d);
+      if (lane >= d) { a += ua; c += uc; }
+    }
+    const int tot0 = __shfl_sync(0xffffffffu, a, 31);
+    const int tot1 = __shfl_sync(0xffffffffu, c, 31);
+    if (lane < nbins) start[lane] = a - t0;
+    if (lane + 32 < nbins) start[lane + 32] = tot0 + c - t1;
+    if (lane == 0) start[nbins] = tot0 + tot1;
+  }
+  __syncthreads();
+  // a tile whose items all share one bin (block mappings: the common case)
+  // maps item k to output k of that bin's segment -- write it straight out
+  int only = -1;
+  for (int b = 0; b < nbins; ++b)
+    if (start[b + 1] - start[b] == kSmallTile) only = b;
+  if (only >= 0) {
+    const long long p0 = pos0[(long long)only * ntiles + blockIdx.x];
+#pragma unroll 4
+    for (int k = threadIdx.x; k < kSmallTile; k += kPartThreads) sink.put(only, p0 + k, base + k);
+    return;
+  }
+  // stable local positions; stage the item offsets in output order
+#pragma unroll
+  for (int j = 0; j < kIPT; ++j) {
+    const int b = bins[j];
+    if (b < 0) continue;
+    int* c = cnt + b * kPartThreads + threadIdx.x;
+    const int r = *c;
+    *c = r + 1;
+    stage[start[b] + r] = (short)(threadIdx.x * kIPT + j);
+  }
+  __syncthreads();
+  // coalesced write-out, one bin segment per warp at a time
+  for (int b = warp; b < nbins; b += kPartWarps) {
+    const int lo = start[b], hi = start[b + 1];
+    if (lo == hi) continue;
+    const long long p0 = pos0[(long long)b * ntiles + blockIdx.x] - lo;
+    for (int k = lo + lane; k < hi; k += 32) sink.put(b, p0 + k, base + stage[k]);
+  }
+}
+
+}  // namespace pmdev

@@ -75,6 +75,13 @@ class PointProgram:
         native.check(native.lib().pm_compile_check(ctypes.byref(self.c_program)),
                      "pm_compile_check")
 
+    def compile_check_fused(self) -> None:
+        """NVRTC-compile the fused map + partition kernels of this program (no GPU)."""
+        from .. import native
+
+        native.check(native.lib().pm_compile_check_fused(ctypes.byref(self.c_program)),
+                     "pm_compile_check_fused")
+
     def plan(self, device: int) -> int:
         from .. import native
 
@@ -99,6 +106,37 @@ class PointProgram:
             native.check(native.lib().pm_map_batch(plan, pts, n, first, out.data_ptr(),
                                                    status.data_ptr(), native.stream_ptr(stream)),
                          "pm_map_batch")
+
+    def map_hist(self, points, n: int, first: int, nbins: int, counts, offsets, status, scratch,
+                 stream=None) -> None:
+        """Fused pass 1 (pm_map_hist): per-processor counts of points [first, first+n)."""
+        from .. import native
+
+        torch = native.require_cuda()
+        dev = counts.device.index if counts.device.index is not None else \
+            torch.cuda.current_device()
+        with torch.cuda.device(dev):
+            plan = self.plan(dev)
+            native.check(native.lib().pm_map_hist(
+                plan, 0 if points is None else points.data_ptr(), n, first, nbins,
+                counts.data_ptr(), offsets.data_ptr(), status.data_ptr(), scratch.data_ptr(),
+                scratch.numel(), native.stream_ptr(stream)), "pm_map_hist")
+
+    def map_scatter(self, points, n: int, first: int, nbins: int, *, out=None, perm=None,
+                    bin_dst=None, index_base: int = 0, status, scratch, stream=None) -> None:
+        """Fused pass 2 (pm_map_scatter): stable slots of every point (after map_hist)."""
+        from .. import native
+
+        torch = native.require_cuda()
+        dev = status.device.index if status.device.index is not None else \
+            torch.cuda.current_device()
+        ptr = (lambda t: 0 if t is None else t.data_ptr())
+        with torch.cuda.device(dev):
+            plan = self.plan(dev)
+            native.check(native.lib().pm_map_scatter(
+                plan, ptr(points), n, first, nbins, ptr(out), ptr(perm), ptr(bin_dst),
+                index_base, status.data_ptr(), scratch.data_ptr(), scratch.numel(),
+                native.stream_ptr(stream)), "pm_map_scatter")
 
     def raise_for(self, status_word: int) -> None:
         """Re-raise the failure a status word encodes (no-op for 'no failure')."""
@@ -264,6 +302,59 @@ class MappingFunction:
             if check:
                 pp.raise_for(int(status.item()))
         return out[:count]
+
+    def map_partition(self, ispace, first: int = 0, count: int | None = None, *,
+                      points=None, with_ids: bool = False, check: bool = True, stream=None):
+        """Ownership lists of a launch in one fused pass pair (K1 + K2 without the
+        id array): the stable partition of points [first, first + count) of
+        `ispace` -- or of the explicit int32 [n, k] `points` -- by processor.
+
+        Same result as `ownership.partition(self.map_ispace(...), P)` (perm holds
+        indices relative to `first`); `with_ids` also returns the processor ids.
+        Launches of more than 64 processors use the unfused K1 + K2 path."""
+        from .. import native
+        from ..ownership import Ownership, partition
+
+        torch = native.require_cuda()
+        ispace = tuple(int(e) for e in ispace)
+        nprocs = self.machine.nodes * self.machine.procs_per_node
+        if points is not None:
+            if points.dtype != torch.int32 or not points.is_cuda or points.dim() != 2:
+                raise ValueError("points must be an int32 CUDA tensor of shape [n, k]")
+            points = points.contiguous()
+            first, count = 0, points.shape[0]
+            dev = points.device
+        else:
+            total = 1
+            for e in ispace:
+                total *= max(e, 0)
+            if count is None:
+                count = total - first
+            if first < 0 or count < 0 or first + count > total:
+                raise ValueError(f"points [{first}, {first + count}) outside the launch of {total}")
+            dev = torch.device("cuda", torch.cuda.current_device())
+        if nprocs > 64:
+            ids = (self.map_points(points, ispace, check=check, stream=stream) if points is not None
+                   else self.map_ispace(ispace, first, count, check=check, stream=stream))
+            own = partition(ids, nprocs, stream=stream, check=check)
+            return (own, ids) if with_ids else own
+        pp = (self.program_for(ispace, implicit=False, k=points.shape[1]) if points is not None
+              else self.program_for(ispace, implicit=True))
+        counts = torch.empty(nprocs, dtype=torch.int64, device=dev)
+        offsets = torch.empty(nprocs, dtype=torch.int64, device=dev)
+        perm = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
+        ids = torch.empty(max(count, 1), dtype=torch.int32, device=dev) if with_ids else None
+        status = torch.full((1,), -1, dtype=torch.int64, device=dev)
+        nbytes = native.lib().pm_map_partition_scratch_bytes(count, nprocs)
+        scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        pfirst = 0 if points is not None else first
+        pp.map_hist(points, count, pfirst, nprocs, counts, offsets, status, scratch, stream)
+        pp.map_scatter(points, count, pfirst, nprocs, out=ids, perm=perm, status=status,
+                       scratch=scratch, stream=stream)
+        if check:
+            pp.raise_for(int(status.item()))
+        own = Ownership(counts, offsets, perm[:count])
+        return (own, ids[:count]) if with_ids else own
 
     def map_points(self, points, ispace, *, out=None, status=None, check: bool = True,
                    stream=None):

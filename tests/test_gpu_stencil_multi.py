@@ -59,3 +59,11 @@ def test_cannon(n):
         pytest.skip(f"needs {n} GPUs")
     v = _run("dist_cannon_check.py", n, 29730 + n)
     assert v["ok"], v
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_sharded_mapping(n):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    v = _run("dist_distmap_check.py", n, 29750 + n)
+    assert v["ok"], v

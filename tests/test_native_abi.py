@@ -56,6 +56,7 @@ def test_codegen_compiles_with_nvrtc(case):
         src = pp.source()
         assert "pm_map_points" in src
         pp.compile_check()
+        pp.compile_check_fused()
 
 
 def test_bad_program_is_rejected():
