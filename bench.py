@@ -299,6 +299,39 @@ def run_cannon(args, rank, world, N, layers, dtype):
     return res
 
 
+def run_circuit(args, rank, world, mapping, pieces_per_gpu=96, npp=5000, wpp=20000,
+                steps=1000, iters=5):
+    """The circuit workload, weak scaling: 96 pieces of 5000 nodes /
+    20000 wires per GPU, 1000 calc_new_currents steps per iteration."""
+    import torch
+
+    from paper_2507_17087_b200.executors.circuit import CircuitSpec, MappedCircuit
+
+    spec = CircuitSpec(pieces_per_gpu * world, npp, wpp, pct_in=95, steps=steps, seed=7)
+    ex = MappedCircuit(spec, mapping=mapping, rank=rank, world=world)
+    cs = torch.cuda.current_stream()
+    ex.step()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cs)
+    for _ in range(iters):
+        ex.step()
+    e1.record(cs)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / iters, world)
+    w = ex.work()
+    wires = sum_over_ranks(w["wires"], world)
+    cross = sum_over_ranks(w["cross_gpu_wires"], world)
+    ops = wires * steps * ex.OPS_PER_WIRE_STEP
+    barrier(world)
+    ex.close()
+    return {"mapping": mapping, "pieces": spec.pieces, "wires": int(wires),
+            "ms_per_iteration": ms, "wire_steps_per_s": wires * steps / (ms * 1e-3),
+            "fp32_ops_per_s": ops / (ms * 1e-3), "cross_gpu_wires": int(cross),
+            "nvlink_bytes_per_iteration": int(8 * cross)}
+
+
 def run_stencil(args, rank, world, rows, cols, mapping, sweeps=20):
     """BASELINE configs[4]: 5-point Jacobi fp32 with the fused NVLink halo exchange."""
     import torch
@@ -456,6 +489,42 @@ def cpu_sample(args, threads=None):
     return C, dt, 2.0 * r * c * S
 
 
+def run_sharded_mapping(args, rank, world):
+    """The 32768^2 stencil launch (configs[4]) mapped + partitioned across the
+    GPUs (distmap.py, fused kernels): with the ownership exchange over NVLink
+    and with each GPU keeping its chunk's lists.  Strong scaling (fixed launch)."""
+    import torch
+
+    from paper_2507_17087_b200 import distmap
+    from paper_2507_17087_b200.dsl import compile_mapper, parse
+    from paper_2507_17087_b200.spaces import MachineShape
+
+    src = ("m = Machine(GPU)\ndef blk(Tuple p, Tuple s):\n"
+           "    q = m.merge(0, 1).decompose(0, s)\n    return q[*(p * q.size / s)]\n"
+           "IndexTaskMap t blk\n")
+    fn = compile_mapper(parse(src), "t", MachineShape("GPU", 1, 8))
+    L = 32768
+    out = {"workload": "32768^2 launch, decompose block mapper, 8 processors, sharded over "
+                       f"{world} GPU(s)", "points": L * L}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for exchange in (True, False):
+        for _ in range(2):
+            distmap.map_launch_sharded(fn, (L, L), rank=rank, world=world, exchange=exchange)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record()
+        reps = 5
+        for _ in range(reps):
+            distmap.map_launch_sharded(fn, (L, L), rank=rank, world=world, exchange=exchange)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1) / reps, world)
+        key = "exchange_to_host_gpu" if exchange else "lists_stay_on_chunk_gpu"
+        out[key] = {"ms": ms, "points_per_s": L * L / (ms * 1e-3)}
+    barrier(world)
+    return out
+
+
 def hot_path_kernels(args):
     """K1 / K2 throughput on config 5 (32768^2 stencil launch, 8-way block mapping)."""
     import torch
@@ -564,6 +633,11 @@ def main_ours(args):
                         max(1, d["halo_cells_per_sweep"] or 1)}
         extra["stencil"] = {"workload": "5-point Jacobi fp32, Mapple block mapping, fused NVLink "
                                         "halo exchange (BASELINE configs[4])", **st}
+    if not args.no_circuit:
+        extra["circuit"] = {"workload": "circuit simulation (configs[4] 'plus circuit sim'), "
+                                        "weak scaling, node exchange fused over NVLink",
+                            "block": run_circuit(args, rank, world, "block"),
+                            "cyclic": run_circuit(args, rank, world, "cyclic")}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         C64, dt, fl = cpu_sample(args)
@@ -587,6 +661,8 @@ def main_ours(args):
         torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_kernels:
         extra["hot_path_kernels"] = hot_path_kernels(args)
+    if not args.no_kernels:
+        extra["sharded_mapping"] = run_sharded_mapping(args, rank, world)
     if rank != 0:
         return
     peak = sustained if dec["ms_per_step"] * args.steps > 1000 else burst
@@ -700,6 +776,7 @@ def main():
     ap.add_argument("--no-3d", action="store_true", help="skip the Johnson / COSMA workloads")
     ap.add_argument("--no-stencil", action="store_true", help="skip the stencil workload")
     ap.add_argument("--no-cannon", action="store_true", help="skip the Cannon / 2.5D workloads")
+    ap.add_argument("--no-circuit", action="store_true", help="skip the circuit workload")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="host seconds spent on the CPU baseline sample")
     args = ap.parse_args()

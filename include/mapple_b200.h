@@ -215,6 +215,40 @@ typedef struct pm_stencil_view {
 } pm_stencil_view;
 int pm_stencil_sweep(const pm_stencil_view* view, int32_t sweep, void* stream);
 
+/* One phase of a circuit-simulation iteration (the paper's Circuit workload,
+ * PAPER.md:495, after the Legion circuit example of Bauer et al. 2012; no
+ * reference code, SURVEY.md §8c "parity unpinned").  Pieces are placed by a
+ * Mapple mapping; node arrays are per GPU; a node reference is
+ * (rank << 27) | slot, resolved through the per-rank pointer tables (peer
+ * pointers for other GPUs, CUDA IPC).  Wire state is structure-of-arrays:
+ * current[s * n_wires + w] (s < SEGMENTS), wire_volt[s * n_wires + w]
+ * (s < SEGMENTS - 1).
+ *   phase 0: calc_new_currents (`steps` iterations) + distribute_charge
+ *            (float atomics into the owning GPU's charge, peer or local);
+ *   phase 1: update_voltages of this GPU's nodes (charge -> voltage, leakage,
+ *            charge reset).
+ * Phases of different GPUs must be separated by a barrier (the executor
+ * orders them with a stream-ordered NCCL all-reduce). */
+#define PM_CIRCUIT_SEGMENTS 10
+#define PM_CIRCUIT_MAX_RANKS 16
+typedef struct pm_circuit_view {
+  int64_t n_wires, n_nodes;  /* this GPU's wires / nodes                       */
+  const int32_t* in_ref;     /* [n_wires] node references                      */
+  const int32_t* out_ref;
+  const float* inductance;   /* [n_wires]                                      */
+  const float* resistance;
+  const float* capacitance;
+  float* current;            /* [SEGMENTS][n_wires]                            */
+  float* wire_volt;          /* [SEGMENTS - 1][n_wires]                        */
+  const float* node_cap;     /* [n_nodes] this GPU's nodes                     */
+  const float* leakage;
+  float* volt[PM_CIRCUIT_MAX_RANKS];   /* per rank: its node voltages / charges */
+  float* charge[PM_CIRCUIT_MAX_RANKS];
+  int32_t rank, steps;
+  float dt;
+} pm_circuit_view;
+int pm_circuit_step(const pm_circuit_view* view, int32_t phase, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

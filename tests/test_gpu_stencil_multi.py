@@ -67,3 +67,11 @@ def test_sharded_mapping(n):
         pytest.skip(f"needs {n} GPUs")
     v = _run("dist_distmap_check.py", n, 29750 + n)
     assert v["ok"], v
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_circuit(n):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    v = _run("dist_circuit_check.py", n, 29770 + n)
+    assert v["ok"], v
