@@ -332,6 +332,39 @@ def run_circuit(args, rank, world, mapping, pieces_per_gpu=96, npp=5000, wpp=200
             "nvlink_bytes_per_iteration": int(8 * cross)}
 
 
+def run_hydro(args, rank, world, mapping, zx=16384, zy=4096, steps=10):
+    """PENNANT-style hydro, strong scaling on a fixed 16384 x 4096-zone
+    mesh (aspect 4:1, where the decompose and heuristic grids differ)."""
+    import torch
+
+    from paper_2507_17087_b200.executors.hydro import HydroSpec, MappedHydro
+
+    ex = MappedHydro(HydroSpec(zx, zy), mapping=mapping, rank=rank, world=world)
+    cs = torch.cuda.current_stream()
+    for _ in range(2):
+        ex.step()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cs)
+    for _ in range(steps):
+        ex.step()
+    e1.record(cs)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    cross = int(sum_over_ranks(ex.cross_corners, world))
+    zones = zx * zy
+    _, _, hbm, _ = peaks()
+    gbs = ex.BYTES_PER_ZONE_STEP * zones / world / (ms * 1e-3) / 1e9
+    barrier(world)
+    ex.close()
+    del ex
+    torch.cuda.empty_cache()
+    return {"mapping": mapping, "zones": zones, "ms_per_step": ms,
+            "zone_steps_per_s": zones / (ms * 1e-3), "cross_gpu_corners": cross,
+            "bytes_per_zone_step": 121, "achieved_gbs_per_gpu": gbs, "frac_hbm": gbs / hbm}
+
+
 def run_stencil(args, rank, world, rows, cols, mapping, sweeps=20):
     """BASELINE configs[4]: 5-point Jacobi fp32 with the fused NVLink halo exchange."""
     import torch
@@ -638,6 +671,13 @@ def main_ours(args):
                                         "weak scaling, node exchange fused over NVLink",
                             "block": run_circuit(args, rank, world, "block"),
                             "cyclic": run_circuit(args, rank, world, "cyclic")}
+    if not args.no_hydro:
+        d = run_hydro(args, rank, world, "decompose")
+        h = run_hydro(args, rank, world, "heuristic")
+        extra["pennant_hydro"] = {"workload": "PENNANT-style Lagrangian hydro, 16384x4096 "
+                                              "quad zones, shared points fused over NVLink",
+                                  "decompose": d, "heuristic": h,
+                                  "speedup": h["ms_per_step"] / d["ms_per_step"]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         C64, dt, fl = cpu_sample(args)
@@ -777,6 +817,7 @@ def main():
     ap.add_argument("--no-stencil", action="store_true", help="skip the stencil workload")
     ap.add_argument("--no-cannon", action="store_true", help="skip the Cannon / 2.5D workloads")
     ap.add_argument("--no-circuit", action="store_true", help="skip the circuit workload")
+    ap.add_argument("--no-hydro", action="store_true", help="skip the PENNANT-style workload")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="host seconds spent on the CPU baseline sample")
     args = ap.parse_args()

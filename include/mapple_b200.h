@@ -249,6 +249,36 @@ typedef struct pm_circuit_view {
 } pm_circuit_view;
 int pm_circuit_step(const pm_circuit_view* view, int32_t phase, void* stream);
 
+/* One phase of a PENNANT-style Lagrangian hydro step (the paper's PENNANT
+ * workload, after Ferenbaugh 2015; no reference code, parity
+ * against oracle/hydro.py).  Quadrilateral zones with counter-clockwise point
+ * references (rank << 27) | slot, z2p[k * n_zones + z]; points per GPU.
+ *   phase 0: zones -- area, PdV energy update with the previous pressure,
+ *            gamma-law EOS, artificial viscosity, corner forces deposited with
+ *            float2 atomics into the owning GPU's fxy (peer or local);
+ *   phase 1: this GPU's points -- acceleration, wall conditions (pbc bit 0:
+ *            x fixed, bit 1: y fixed), velocity / position update, force reset.
+ * Phases of different GPUs must be separated by a barrier. */
+#define PM_HYDRO_MAX_RANKS 16
+typedef struct pm_hydro_view {
+  int64_t n_zones, n_points;
+  const int32_t* z2p;        /* [4][n_zones] point references                  */
+  const float* zm;           /* [n_zones] zone mass                            */
+  float* ze;                 /* specific internal energy                       */
+  float* za;                 /* area after the last step                       */
+  float* zpe;                /* p + q of the last step (0 before the first)    */
+  const float* pm;           /* [n_points] point mass                          */
+  const int8_t* pbc;         /* [n_points] wall flags                          */
+  float* px[PM_HYDRO_MAX_RANKS];
+  float* py[PM_HYDRO_MAX_RANKS];
+  float* ux[PM_HYDRO_MAX_RANKS];
+  float* uy[PM_HYDRO_MAX_RANKS];
+  float* fxy[PM_HYDRO_MAX_RANKS];     /* interleaved (fx, fy) per point  */
+  int32_t rank;
+  float dt, gamma, cq;
+} pm_hydro_view;
+int pm_hydro_step(const pm_hydro_view* view, int32_t phase, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

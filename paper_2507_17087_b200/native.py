@@ -114,6 +114,7 @@ def stream_ptr(stream=None) -> int:
 
 SIGNATURES["pm_stencil_sweep"] = (ctypes.c_int, [ctypes.c_void_p, _I32, _VP])
 SIGNATURES["pm_circuit_step"] = (ctypes.c_int, [ctypes.c_void_p, _I32, _VP])
+SIGNATURES["pm_hydro_step"] = (ctypes.c_int, [ctypes.c_void_p, _I32, _VP])
 SIGNATURES["pm_map_partition_scratch_bytes"] = (ctypes.c_size_t, [_I64, _I32])
 SIGNATURES["pm_compile_check_fused"] = (ctypes.c_int, [ctypes.POINTER(PmProgram)])
 SIGNATURES["pm_map_hist"] = (ctypes.c_int, [_VP, _VP, _I64, _I64, _I32, _VP, _VP, _VP, _VP,

@@ -75,3 +75,11 @@ def test_circuit(n):
         pytest.skip(f"needs {n} GPUs")
     v = _run("dist_circuit_check.py", n, 29770 + n)
     assert v["ok"], v
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_hydro(n):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    v = _run("dist_hydro_check.py", n, 29790 + n)
+    assert v["ok"], v
