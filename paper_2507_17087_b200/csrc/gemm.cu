@@ -968,7 +968,15 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_h);
     }
-    if (lane == 0) bulk_wait0();
+    if (lane == 0) {
+      // the TMA stores / reduce-adds (async proxy, possibly into a peer GPU's C) have
+      // completed; publish them at system scope before the kernel retires, so work
+      // ordered after this kernel on any GPU (e.g. a stream-ordered NCCL barrier)
+      // observes them
+      bulk_wait0();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence_system();
+    }
   }
 
   tc_fence_before();

@@ -184,7 +184,10 @@ class MappedCannon:
         buf = self.step_i % 2
         self.step_i += 1
         if c > 1:
-            self.C[1 - buf].zero_()
+            # the layers' adds into C[buf] date from two steps ago and all finished before
+            # the previous step's barriers; the schedule's first barrier orders this zeroing
+            # before any peer adds into it again
+            self.C[buf].zero_()
         moved = 0
         first = True  # the first local product overwrites C (Cannon); 2.5D always adds
         for op in cannon_schedule(q, c, self.coord):

@@ -158,8 +158,12 @@ class MappedGemm3D:
         buf = self.step_i % 2
         self.step_i += 1
         if self.reduce:
-            self.C[1 - buf].zero_()   # consumed: the previous step's result was in C[1-buf]
-            self._barrier()           # every GPU zeroed its C[buf] two steps ago and is here
+            # C[buf] was last added into two steps ago; every GPU finished those GEMMs
+            # before it joined the previous step's barrier, which we passed: zero it now,
+            # and only then (barrier) may the peers add into it.  C[1-buf] -- the previous
+            # step's result -- stays intact during this step.
+            self.C[buf].zero_()
+            self._barrier()
         for s in self.streams:
             s.wait_event(self.done)
         for name, q, (r0, r1), si, ev in self.pulls:
