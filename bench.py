@@ -593,6 +593,18 @@ def hot_path_kernels(args):
     e1.record()
     torch.cuda.synchronize()
     k2_ms = e0.elapsed_time(e1) / 5
+    # K3: halo transfer lists of the same 8-way block ownership (h = 1)
+    from paper_2507_17087_b200.transfer import halo_lists
+
+    tl = halo_lists(out, (L, L), (1, 1), 8)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(3):
+        tl = halo_lists(out, (L, L), (1, 1), 8)
+    e1.record()
+    torch.cuda.synchronize()
+    k3_ms = e0.elapsed_time(e1) / 3
+    k3_entries = tl.total
     # K1+K2 fused: two passes over the launch, ids never stored (4 B/pt: the perm write)
     fn.map_partition((L, L), check=False)
     torch.cuda.synchronize()
@@ -617,6 +629,10 @@ def hot_path_kernels(args):
             "k2_partition": {"ms": k2_ms, "bytes_per_point": k2_bpp,
                              "uniform_tile_fraction": uniform, "achieved_gbs": k2_gbs,
                              "frac_hbm": k2_gbs / hbm},
+            "k3_halo_lists": {"ms": k3_ms, "entries": k3_entries,
+                              "bytes": 4 * n + 9 * k3_entries,
+                              "achieved_gbs": (4 * n + 9 * k3_entries) / (k3_ms * 1e-3) / 1e9,
+                              "frac_hbm": (4 * n + 9 * k3_entries) / (k3_ms * 1e-3) / 1e9 / hbm},
             "k12_fused_map_partition": {"ms": k12_ms, "points_per_s": n / (k12_ms * 1e-3),
                                         "bytes_per_point": 4, "achieved_gbs": k12_gbs,
                                         "frac_hbm": k12_gbs / hbm,

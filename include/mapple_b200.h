@@ -161,6 +161,24 @@ int pm_halo_lists(const int32_t* owner, const int64_t* ext, int32_t rank,
                   const int32_t* halo, int32_t nprocs, int64_t* pair_counts,
                   int64_t* pair_offsets, int64_t* cells, int8_t* dims, void* scratch,
                   size_t scratch_bytes, void* stream);
+/* The same lists by compaction (what transfer.halo_lists uses; halo entries are
+ * sparse, so no per-(pair, tile) histogram is built):
+ *   pm_halo_count    pair_counts[nprocs^2] and, in tile_scratch
+ *                    (pm_halo_tile_scratch_bytes), each 8192-slot tile's output
+ *                    offset;
+ *   pm_halo_compact  every entry as (pair key, slot index = cell * 2R + 2n + (s>0))
+ *                    in slot order into keys / slots [sum of pair_counts];
+ *   (pm_partition of keys into nprocs^2 bins -> perm, counts, offsets)
+ *   pm_halo_gather   cells[j] / dims[j] of slots[perm[j]] (dims nullable). */
+size_t pm_halo_tile_scratch_bytes(const int64_t* ext, int32_t rank);
+int pm_halo_count(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
+                  int32_t nprocs, int64_t* pair_counts, void* tile_scratch, size_t bytes,
+                  void* stream);
+int pm_halo_compact(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
+                    int32_t nprocs, void* tile_scratch, int32_t* keys, int64_t* slots,
+                    void* stream);
+int pm_halo_gather(const int32_t* perm, const int64_t* slots, int64_t n, int32_t rank,
+                   int64_t* cells, int8_t* dims, void* stream);
 
 /* C[M,N] (+)= A[M,K] * B[K,N] on the tcgen05 tensor cores, bf16 inputs, fp32
  * accumulation.  A is row-major (K contiguous, lda >= K); B is given

@@ -22,6 +22,9 @@
 namespace pm {
 namespace {
 
+// I: index arithmetic type -- 32-bit whenever the slot count allows (integer
+// division by the runtime extents dominates the key's cost)
+template <typename I>
 struct HaloKey {
   const int* __restrict__ owner;
   long long ext[3];
@@ -29,24 +32,89 @@ struct HaloKey {
   int halo[3];
   int rank;
   int nprocs;
-  static constexpr bool kVec4 = false;
+  bool vec_ok;  // 2-D grid: the 4 slots of a cell are 4 consecutive items -> keys4
+  bool unit_halo;     // 2-D with h = (1, 1)
+  bool small_pairs;   // nprocs^2 < 128: keys fit the int8 lanes of keys4
+  double inv_cols;    // 1 / ext[1]
+  unsigned div_m, div_s;  // magic multiplier / shift for n / ext[1] (32-bit keys)
+  bool div_one;           // ext[1] == 1
+  static constexpr bool kVec4 = true;
   static constexpr bool kPeek = false;
   __device__ __forceinline__ void uniform(long long, int, int) const {}
+  // the four slots (up, down, left, right) of cell i / 4 of a 2-D grid: one index
+  // decomposition and one owner load per cell, neighbours from L1/L2
+  __device__ __forceinline__ int keys4(long long i) const {
+    const I cell = (I)i >> 2;
+    const I cols = (I)ext[1];
+    I r;
+    if constexpr (sizeof(I) == 4) {
+      // row = cell / cols by multiply-high with the host's magic number (exact for
+      // every 32-bit numerator; branch-free round-up method)
+      if (div_one) {
+        r = cell;
+      } else {
+        const unsigned t = __umulhi(div_m, cell);
+        r = (t + ((cell - t) >> 1)) >> div_s;
+      }
+    } else {
+      // 64-bit slot space: double reciprocal, corrected to the exact quotient
+      r = (I)((double)cell * inv_cols);
+      if (r * cols > cell) --r;
+      else if ((r + 1) * cols <= cell) ++r;
+    }
+    const I c = cell - r * cols;
+    const int o = __ldg(owner + cell);
+    if (o < 0 || o >= nprocs) return -1;  // all four slots empty (0xFF bytes)
+    if (unit_halo) {  // h = (1, 1): the four direct neighbours
+      const int qs[4] = {r > 0 ? __ldg(owner + (cell - cols)) : o,
+                         (long long)r + 1 < ext[0] ? __ldg(owner + (cell + cols)) : o,
+                         c > 0 ? __ldg(owner + (cell - 1)) : o,
+                         (long long)c + 1 < ext[1] ? __ldg(owner + (cell + 1)) : o};
+      int packed = 0;
+#pragma unroll
+      for (int dd = 0; dd < 4; ++dd) {
+        const int q = qs[dd];
+        const int key = (q == o || q < 0 || q >= nprocs) ? -1 : o * nprocs + q;
+        packed |= (key & 0xFF) << (8 * dd);
+      }
+      return packed;
+    }
+    int packed = 0;
+#pragma unroll
+    for (int dd = 0; dd < 4; ++dd) {
+      const int n = dd >> 1;
+      const int dir = (dd & 1) ? 1 : -1;
+      const long long x = n == 0 ? (long long)r : (long long)c;
+      const long long st = n == 0 ? (long long)cols : 1;
+      int key = -1;
+      for (int j = 1; j <= halo[n]; ++j) {
+        const long long y = x + dir * j;
+        if (y < 0 || y >= ext[n]) break;
+        const int q = __ldg(owner + (long long)cell + (long long)dir * j * st);
+        if (q != o) {
+          key = (q < 0 || q >= nprocs) ? -1 : o * nprocs + q;
+          break;
+        }
+      }
+      packed |= (key & 0xFF) << (8 * dd);
+    }
+    return packed;
+  }
   __device__ __forceinline__ int operator()(long long i) const {
-    const int slots = 2 * rank;
-    const long long cell = i / slots;
-    const int dd = (int)(i - cell * slots);
+    const I slots = (I)(2 * rank);
+    const I cell = (I)i / slots;
+    const int dd = (int)((I)i - cell * slots);
     const int n = dd >> 1;
     const int dir = (dd & 1) ? 1 : -1;
     const int h = halo[n];
     if (h <= 0) return -1;
-    const long long x = (cell / stride[n]) % ext[n];
+    const I x = (cell / (I)stride[n]) % (I)ext[n];
     const int o = __ldg(owner + cell);
     if (o < 0 || o >= nprocs) return -1;
     for (int j = 1; j <= h; ++j) {
-      const long long y = x + dir * j;
+      const long long y = (long long)x + dir * j;
       if (y < 0 || y >= ext[n]) return -1;
-      const int q = __ldg(owner + cell + (long long)dir * j * stride[n]);
+      const int q = __ldg(owner + (long long)cell + (long long)dir * j * stride[n]);
       if (q != o) return (q < 0 || q >= nprocs) ? -1 : o * nprocs + q;
     }
     return -1;
@@ -67,13 +135,16 @@ struct HaloSink {
   }
 };
 
+template <typename I>
 bool make_key(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
-              int32_t nprocs, HaloKey* k, long long* ncells) {
+              int32_t nprocs, HaloKey<I>* k, long long* ncells) {
   if (rank < 1 || rank > 3 || nprocs < 1 || nprocs > 64 || !ext || !halo) return false;
-  *k = HaloKey{};
+  *k = HaloKey<I>{};
   k->owner = owner;
   k->rank = rank;
   k->nprocs = nprocs;
+  k->vec_ok = rank == 2;
+  k->small_pairs = nprocs * nprocs < 128;
   long long st = 1;
   for (int m = rank - 1; m >= 0; --m) {
     if (ext[m] < 1 || halo[m] < 0) return false;
@@ -83,7 +154,306 @@ bool make_key(const int32_t* owner, const int64_t* ext, int32_t rank, const int3
     st *= ext[m];
   }
   *ncells = st;
+  if (rank == 2) {
+    k->unit_halo = halo[0] == 1 && halo[1] == 1;
+    k->inv_cols = 1.0 / (double)ext[1];
+    // n / d = (t + ((n - t) >> 1)) >> (l - 1), t = umulhi(m, n), l = ceil(log2 d),
+    // m = floor(2^32 (2^l - d) / d) + 1  (d >= 2; valid for all 32-bit n)
+    const unsigned long long d = (unsigned long long)ext[1];
+    k->div_one = d == 1;
+    if (d >= 2 && d <= 0xFFFFFFFFull) {
+      unsigned l = 0;
+      while ((1ull << l) < d) ++l;
+      k->div_m = (unsigned)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+      k->div_s = l - 1;
+    }
+  }
   return true;
+}
+
+// ---- K3 by compaction (transfer.halo_lists) ---------------------------------------
+//
+// Halo entries are sparse (cells next to an ownership boundary), so instead of a
+// per-(pair, tile) histogram the lists are built in three steps:
+//   k_halo_count    per 8192-slot tile: number of entries; per-pair totals by
+//                   shared then global atomics (non-empty tiles only)
+//   exclusive scan  of the tile counts -> each tile's first output slot
+//   k_halo_compact  non-empty tiles only: warp-shuffle + shared-memory prefix
+//                   sums place every entry (pair key, slot index) in slot order
+// then K2 stably partitions the compacted keys by pair and k_halo_gather emits
+// (cell, dim) in that order -- the same lists as the single-pass partition.
+constexpr int kHaloTile = 8192;  // slots per tile: 8 rounds of 256 threads x 4
+constexpr int kHaloRounds = kHaloTile / (4 * kPartThreads);
+
+template <class Key>
+__device__ __forceinline__ void halo_keys4(const Key& key, long long i0, long long n, int (&k)[4]) {
+  if (key.vec_ok && key.small_pairs && i0 + 3 < n) {
+    const int packed = key.keys4(i0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) k[q] = (int)(signed char)(packed >> (8 * q));
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) k[q] = i0 + q < n ? key(i0 + q) : -1;
+  }
+}
+
+template <class Key>
+__global__ void __launch_bounds__(kPartThreads)
+k_halo_count(Key key, long long n, int npairs, long long* __restrict__ tile_cnt,
+             unsigned long long* __restrict__ pair_cnt) {
+  extern __shared__ int sp[];  // [npairs]
+  __shared__ int s_tot;
+  for (int b = threadIdx.x; b < npairs; b += kPartThreads) sp[b] = 0;
+  if (threadIdx.x == 0) s_tot = 0;
+  __syncthreads();
+  const long long base = (long long)blockIdx.x * kHaloTile;
+  int c = 0;
+  for (int r = 0; r < kHaloRounds; ++r) {
+    int k[4];
+    halo_keys4(key, base + (long long)r * 4 * kPartThreads + 4 * threadIdx.x, n, k);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (k[q] >= 0) {
+        ++c;
+        atomicAdd(&sp[k[q]], 1);
+      }
+  }
+  for (int d = 16; d; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_tot, c);
+  __syncthreads();
+  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = s_tot;
+  if (s_tot)
+    for (int b = threadIdx.x; b < npairs; b += kPartThreads)
+      if (sp[b]) atomicAdd(pair_cnt + b, (unsigned long long)sp[b]);
+}
+
+template <class Key>
+__global__ void __launch_bounds__(kPartThreads)
+k_halo_compact(Key key, long long n, long long ntiles, const long long* __restrict__ tile_off,
+               const long long* __restrict__ total, int* __restrict__ out_key,
+               long long* __restrict__ out_slot) {
+  const long long t = blockIdx.x;
+  const long long lo = tile_off[t], hi = t + 1 < ntiles ? tile_off[t + 1] : *total;
+  if (lo == hi) return;
+  __shared__ int s_warp[kPartWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long base = t * kHaloTile;
+  long long running = lo;
+  for (int r = 0; r < kHaloRounds; ++r) {
+    const long long i0 = base + (long long)r * 4 * kPartThreads + 4 * threadIdx.x;
+    int k[4];
+    halo_keys4(key, i0, n, k);
+    const int c = (k[0] >= 0) + (k[1] >= 0) + (k[2] >= 0) + (k[3] >= 0);
+    int incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += u;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < kPartWarps; ++w) {
+      const int v = s_warp[w];
+      before += w < warp ? v : 0;
+      all += v;
+    }
+    long long pos = running + before + incl - c;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (k[q] >= 0) {
+        out_key[pos] = k[q];
+        out_slot[pos] = i0 + q;
+        ++pos;
+      }
+    running += all;
+    __syncthreads();
+  }
+}
+
+__global__ void k_halo_gather(const int* __restrict__ perm, const long long* __restrict__ slot,
+                              long long n, int slots, long long* __restrict__ cells,
+                              signed char* __restrict__ dims) {
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    const long long s = slot[perm[j]];
+    const long long c = s / slots;
+    cells[j] = c;
+    if (dims) dims[j] = (signed char)(s - c * slots);
+  }
+}
+
+// ---- 2-D, h = (1, 1), cols % 4 == 0: four cells per thread from int4 loads ------------
+//
+// The common stencil case.  A thread takes 4 consecutive cells of one row (16-byte
+// loads of the row and of the rows above and below, two scalar loads for the left
+// and right ends) and derives the 16 slots' keys in registers; most groups have no
+// entry at all and cost one comparison.  Tiles are the same 8192 slots (2048 cells,
+// 2 groups per thread) as the generic kernels, so the scan is shared.
+struct Halo2D {
+  const int* __restrict__ owner;
+  unsigned rows, cols, div_m, div_s;
+  int nprocs;
+  // keys of the 16 slots of the 4 cells starting at cell0 (slot order: cell, dd);
+  // returns the number of entries
+  __device__ __forceinline__ int keys(unsigned cell0, int (&k)[16]) const {
+    const unsigned t = __umulhi(div_m, cell0);
+    const unsigned r = (t + ((cell0 - t) >> 1)) >> div_s;
+    const unsigned c0 = cell0 - r * cols;
+    const int4 cur = __ldg(reinterpret_cast<const int4*>(owner + cell0));
+    const int4 up = r > 0 ? __ldg(reinterpret_cast<const int4*>(owner + cell0 - cols)) : cur;
+    const int4 dn = r + 1 < rows ? __ldg(reinterpret_cast<const int4*>(owner + cell0 + cols)) : cur;
+    const int lf = c0 > 0 ? __ldg(owner + cell0 - 1) : cur.x;
+    const int rt = c0 + 4 < cols ? __ldg(owner + cell0 + 4) : cur.w;
+    const int o[4] = {cur.x, cur.y, cur.z, cur.w};
+    const int q[4][4] = {{up.x, dn.x, lf, cur.y},
+                         {up.y, dn.y, cur.x, cur.z},
+                         {up.z, dn.z, cur.y, cur.w},
+                         {up.w, dn.w, cur.z, rt}};
+    int n = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int dd = 0; dd < 4; ++dd) {
+        const int qq = q[j][dd];
+        const bool e = qq != o[j] && (unsigned)qq < (unsigned)nprocs &&
+                       (unsigned)o[j] < (unsigned)nprocs;
+        k[j * 4 + dd] = e ? o[j] * nprocs + qq : -1;
+        n += e;
+      }
+    return n;
+  }
+};
+
+__global__ void __launch_bounds__(kPartThreads)
+k_halo2d_count(Halo2D h, long long ncells, int npairs, long long* __restrict__ tile_cnt,
+               unsigned long long* __restrict__ pair_cnt) {
+  extern __shared__ int sp[];
+  __shared__ int s_tot;
+  for (int b = threadIdx.x; b < npairs; b += kPartThreads) sp[b] = 0;
+  if (threadIdx.x == 0) s_tot = 0;
+  __syncthreads();
+  const long long base = (long long)blockIdx.x * (kHaloTile / 4);
+  int c = 0;
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const long long cell0 = base + (long long)(g * kPartThreads + threadIdx.x) * 4;
+    if (cell0 >= ncells) break;
+    int k[16];
+    const int n = h.keys((unsigned)cell0, k);
+    if (n) {
+      c += n;
+#pragma unroll
+      for (int s = 0; s < 16; ++s)
+        if (k[s] >= 0) atomicAdd(&sp[k[s]], 1);
+    }
+  }
+  for (int d = 16; d; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_tot, c);
+  __syncthreads();
+  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = s_tot;
+  if (s_tot)
+    for (int b = threadIdx.x; b < npairs; b += kPartThreads)
+      if (sp[b]) atomicAdd(pair_cnt + b, (unsigned long long)sp[b]);
+}
+
+__global__ void __launch_bounds__(kPartThreads)
+k_halo2d_compact(Halo2D h, long long ncells, long long ntiles,
+                 const long long* __restrict__ tile_off, const long long* __restrict__ total,
+                 int* __restrict__ out_key, long long* __restrict__ out_slot) {
+  const long long t = blockIdx.x;
+  const long long lo = tile_off[t], hi = t + 1 < ntiles ? tile_off[t + 1] : *total;
+  if (lo == hi) return;
+  __shared__ int s_warp[kPartWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long base = t * (kHaloTile / 4);
+  long long running = lo;
+#pragma unroll 1
+  for (int g = 0; g < 2; ++g) {
+    const long long cell0 = base + (long long)(g * kPartThreads + threadIdx.x) * 4;
+    int k[16];
+    const int c = cell0 < ncells ? h.keys((unsigned)cell0, k) : 0;
+    int incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += u;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < kPartWarps; ++w) {
+      const int v = s_warp[w];
+      before += w < warp ? v : 0;
+      all += v;
+    }
+    if (c) {
+      long long pos = running + before + incl - c;
+#pragma unroll
+      for (int s = 0; s < 16; ++s)
+        if (k[s] >= 0) {
+          out_key[pos] = k[s];
+          out_slot[pos] = cell0 * 4 + s;
+          ++pos;
+        }
+    }
+    running += all;
+    __syncthreads();
+  }
+}
+
+bool make_halo2d(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
+                 int32_t nprocs, Halo2D* h) {
+  if (rank != 2 || halo[0] != 1 || halo[1] != 1 || ext[1] % 4 != 0 || ext[1] < 4 ||
+      (uintptr_t)owner % 16 != 0 || ext[0] * ext[1] * 4 > (1LL << 32) || nprocs < 1 ||
+      nprocs > 64)
+    return false;
+  h->owner = owner;
+  h->rows = (unsigned)ext[0];
+  h->cols = (unsigned)ext[1];
+  h->nprocs = nprocs;
+  const unsigned long long d = (unsigned long long)ext[1];
+  unsigned l = 0;
+  while ((1ull << l) < d) ++l;
+  h->div_m = (unsigned)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+  h->div_s = l - 1;
+  return true;
+}
+
+size_t halo_tile_bytes(long long ntiles) {
+  return (size_t)(((ntiles * 8 + 255) / 256) * 256) + scan_scratch_bytes(ntiles);
+}
+
+template <class Key>
+int halo_count(const Key& key, long long n, int npairs, long long* pair_cnt, void* scratch,
+               size_t bytes, cudaStream_t s) {
+  const long long ntiles = (n + kHaloTile - 1) / kHaloTile;
+  if (bytes < halo_tile_bytes(ntiles)) return set_error("pm_halo_count: scratch too small"),
+                                               PM_ERR_INVALID;
+  PM_CUDA_TRY(cudaMemsetAsync(pair_cnt, 0, sizeof(long long) * npairs, s));
+  if (ntiles == 0) return PM_OK;
+  long long* tile = reinterpret_cast<long long*>(scratch);
+  void* scan_tmp = reinterpret_cast<char*>(scratch) + ((ntiles * 8 + 255) / 256) * 256;
+  k_halo_count<Key><<<(unsigned)ntiles, kPartThreads, sizeof(int) * npairs, s>>>(
+      key, n, npairs, tile, reinterpret_cast<unsigned long long*>(pair_cnt));
+  PM_CUDA_TRY(cudaGetLastError());
+  return exclusive_scan_i64(tile, ntiles, scan_tmp, s);
+}
+
+template <class Key>
+int halo_compact(const Key& key, long long n, void* scratch, int* keys, long long* slots_out,
+                 cudaStream_t s) {
+  const long long ntiles = (n + kHaloTile - 1) / kHaloTile;
+  if (ntiles == 0) return PM_OK;
+  const long long* tile = reinterpret_cast<const long long*>(scratch);
+  const long long* total = reinterpret_cast<const long long*>(
+      reinterpret_cast<char*>(scratch) + ((ntiles * 8 + 255) / 256) * 256);
+  k_halo_compact<Key><<<(unsigned)ntiles, kPartThreads, 0, s>>>(key, n, ntiles, tile, total, keys,
+                                                               slots_out);
+  PM_CUDA_TRY(cudaGetLastError());
+  return PM_OK;
 }
 
 }  // namespace
@@ -101,18 +471,117 @@ size_t pm_halo_scratch_bytes(const int64_t* ext, int32_t rank, int32_t nprocs) {
 int pm_halo_lists(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
                   int32_t nprocs, int64_t* pair_counts, int64_t* pair_offsets, int64_t* cells,
                   int8_t* dims, void* scratch, size_t scratch_bytes, void* stream) {
-  pm::HaloKey key;
   long long ncells = 0;
+  pm::HaloKey<unsigned long long> key64;
   if (!owner || !pair_counts || !pair_offsets ||
-      !pm::make_key(owner, ext, rank, halo, nprocs, &key, &ncells))
+      !pm::make_key(owner, ext, rank, halo, nprocs, &key64, &ncells))
     return pm::set_error("pm_halo_lists: bad arguments (rank 1..3, nprocs 1..64)"),
            PM_ERR_INVALID;
   pm::HaloSink sink{reinterpret_cast<long long*>(cells), reinterpret_cast<signed char*>(dims),
                     2 * rank};
-  return pm::stable_partition(key, sink, cells != nullptr, ncells * 2 * rank, nprocs * nprocs,
+  const long long items = ncells * 2 * rank;
+  if (items <= (1LL << 32)) {  // 32-bit slot arithmetic (item indices < 2^32)
+    pm::HaloKey<unsigned> key32;
+    pm::make_key(owner, ext, rank, halo, nprocs, &key32, &ncells);
+    return pm::stable_partition(key32, sink, cells != nullptr, items, nprocs * nprocs,
+                                reinterpret_cast<long long*>(pair_counts),
+                                reinterpret_cast<long long*>(pair_offsets), scratch,
+                                scratch_bytes, (cudaStream_t)stream);
+  }
+  return pm::stable_partition(key64, sink, cells != nullptr, items, nprocs * nprocs,
                               reinterpret_cast<long long*>(pair_counts),
                               reinterpret_cast<long long*>(pair_offsets), scratch, scratch_bytes,
                               (cudaStream_t)stream);
+}
+
+size_t pm_halo_tile_scratch_bytes(const int64_t* ext, int32_t rank) {
+  if (!ext || rank < 1 || rank > 3) return 256;
+  long long cells = 1;
+  for (int m = 0; m < rank; ++m) cells *= ext[m];
+  const long long ntiles = (cells * 2 * rank + pm::kHaloTile - 1) / pm::kHaloTile;
+  return pm::halo_tile_bytes(ntiles);
+}
+
+int pm_halo_count(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
+                  int32_t nprocs, int64_t* pair_counts, void* tile_scratch, size_t bytes,
+                  void* stream) {
+  long long ncells = 0;
+  pm::HaloKey<unsigned long long> key64;
+  if (!owner || !pair_counts || !tile_scratch ||
+      !pm::make_key(owner, ext, rank, halo, nprocs, &key64, &ncells))
+    return pm::set_error("pm_halo_count: bad arguments (rank 1..3, nprocs 1..64)"),
+           PM_ERR_INVALID;
+  const long long items = ncells * 2 * rank;
+  auto* pc = reinterpret_cast<long long*>(pair_counts);
+  pm::Halo2D h2;
+  if (pm::make_halo2d(owner, ext, rank, halo, nprocs, &h2)) {
+    const long long ntiles = (items + pm::kHaloTile - 1) / pm::kHaloTile;
+    if (bytes < pm::halo_tile_bytes(ntiles))
+      return pm::set_error("pm_halo_count: scratch too small"), PM_ERR_INVALID;
+    cudaStream_t s = (cudaStream_t)stream;
+    PM_CUDA_TRY(cudaMemsetAsync(pc, 0, sizeof(long long) * nprocs * nprocs, s));
+    long long* tile = reinterpret_cast<long long*>(tile_scratch);
+    pm::k_halo2d_count<<<(unsigned)ntiles, pm::kPartThreads, sizeof(int) * nprocs * nprocs, s>>>(
+        h2, ncells, nprocs * nprocs, tile, reinterpret_cast<unsigned long long*>(pc));
+    PM_CUDA_TRY(cudaGetLastError());
+    return pm::exclusive_scan_i64(tile, ntiles,
+                                  reinterpret_cast<char*>(tile_scratch) +
+                                      ((ntiles * 8 + 255) / 256) * 256,
+                                  s);
+  }
+  if (items <= (1LL << 32)) {
+    pm::HaloKey<unsigned> key32;
+    pm::make_key(owner, ext, rank, halo, nprocs, &key32, &ncells);
+    return pm::halo_count(key32, items, nprocs * nprocs, pc, tile_scratch, bytes,
+                          (cudaStream_t)stream);
+  }
+  return pm::halo_count(key64, items, nprocs * nprocs, pc, tile_scratch, bytes,
+                        (cudaStream_t)stream);
+}
+
+int pm_halo_compact(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
+                    int32_t nprocs, void* tile_scratch, int32_t* keys, int64_t* slots,
+                    void* stream) {
+  long long ncells = 0;
+  pm::HaloKey<unsigned long long> key64;
+  if (!owner || !tile_scratch || !keys || !slots ||
+      !pm::make_key(owner, ext, rank, halo, nprocs, &key64, &ncells))
+    return pm::set_error("pm_halo_compact: bad arguments"), PM_ERR_INVALID;
+  const long long items = ncells * 2 * rank;
+  auto* so = reinterpret_cast<long long*>(slots);
+  pm::Halo2D h2;
+  if (pm::make_halo2d(owner, ext, rank, halo, nprocs, &h2)) {
+    const long long ntiles = (items + pm::kHaloTile - 1) / pm::kHaloTile;
+    if (ntiles == 0) return PM_OK;
+    const long long* tile = reinterpret_cast<const long long*>(tile_scratch);
+    const long long* total = reinterpret_cast<const long long*>(
+        reinterpret_cast<char*>(tile_scratch) + ((ntiles * 8 + 255) / 256) * 256);
+    pm::k_halo2d_compact<<<(unsigned)ntiles, pm::kPartThreads, 0, (cudaStream_t)stream>>>(
+        h2, ncells, ntiles, tile, total, keys, so);
+    PM_CUDA_TRY(cudaGetLastError());
+    return PM_OK;
+  }
+  if (items <= (1LL << 32)) {
+    pm::HaloKey<unsigned> key32;
+    pm::make_key(owner, ext, rank, halo, nprocs, &key32, &ncells);
+    return pm::halo_compact(key32, items, tile_scratch, keys, so, (cudaStream_t)stream);
+  }
+  return pm::halo_compact(key64, items, tile_scratch, keys, so, (cudaStream_t)stream);
+}
+
+int pm_halo_gather(const int32_t* perm, const int64_t* slots, int64_t n, int32_t rank,
+                   int64_t* cells, int8_t* dims, void* stream) {
+  if (n < 0 || rank < 1 || rank > 3 || (n > 0 && (!perm || !slots || !cells)))
+    return pm::set_error("pm_halo_gather: bad arguments"), PM_ERR_INVALID;
+  if (n == 0) return PM_OK;
+  long long blocks = (n + 255) / 256;
+  const long long cap = (long long)pm::num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  pm::k_halo_gather<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      perm, reinterpret_cast<const long long*>(slots), n, 2 * rank,
+      reinterpret_cast<long long*>(cells), reinterpret_cast<signed char*>(dims));
+  PM_CUDA_TRY(cudaGetLastError());
+  return PM_OK;
 }
 
 }  // extern "C"

@@ -69,7 +69,7 @@ int pm_map_hist(pm_plan* plan, const int32_t* points, int64_t n, int64_t first, 
   long long ntiles = (n + pm::kSmallTile - 1) / pm::kSmallTile;
   const long long len = ntiles * nbins;
   long long* hist = reinterpret_cast<long long*>(scratch);
-  void* scan_tmp = reinterpret_cast<char*>(scratch) + len * 8;
+  void* scan_tmp = reinterpret_cast<char*>(scratch) + pm::small_scan_offset(ntiles, nbins);
   const size_t smem = pm::small_hist_smem(nbins);
   if ((rc = set_smem(plan->fn_hist, smem))) return rc;
   const int32_t* pts = points;

@@ -83,11 +83,24 @@ __device__ __forceinline__ void small_keys(const Key& key, long long base, long 
 // keys it evaluates (coalesced order) and flushes a run into its warp's
 // shared histogram with one atomic when the bin changes -- block mappings
 // flush once per thread.  shared: h[kPartWarps][nbins]
+//
+// Scratch layout shared with the host (stable_partition.cuh): hist[nbins][ntiles]
+// (int64, scanned in place into output slots), then tile_info[ntiles] (int32):
+// the single bin of a full tile, kTileEmpty (no output) or kTileMixed.
+constexpr int kTileMixed = -1;
+constexpr int kTileEmpty = -2;
+__device__ __forceinline__ const int* tile_info_of(const long long* hist, int nbins,
+                                                   long long ntiles) {
+  return reinterpret_cast<const int*>(hist + (long long)nbins * ntiles);
+}
+
 template <class Key>
 __device__ __forceinline__ void small_hist_body(const Key& key, long long n, int nbins,
                                                 long long ntiles, long long* __restrict__ hist,
                                                 int* smem_words) {
   int* h = smem_words;
+  __shared__ int s_only, s_any;
+  if (threadIdx.x == 0) s_only = kTileMixed, s_any = 0;
   for (int b = threadIdx.x; b < kPartWarps * nbins; b += kPartThreads) h[b] = 0;
   __syncthreads();
   const long long base = (long long)blockIdx.x * kSmallTile;
@@ -146,6 +159,17 @@ __device__ __forceinline__ void small_hist_body(const Key& key, long long n, int
 #pragma unroll
     for (int w = 0; w < kPartWarps; ++w) sum += h[w * nbins + b];
     hist[(long long)b * ntiles + blockIdx.x] = sum;
+    if (sum) s_any = 1;
+    if (sum == kSmallTile) s_only = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // the last (possibly partial) tile always takes the general path
+    const int info = blockIdx.x + 1 == ntiles ? kTileMixed
+                     : s_only >= 0            ? s_only
+                     : s_any                  ? kTileMixed
+                                              : kTileEmpty;
+    const_cast<int*>(tile_info_of(hist, nbins, ntiles))[blockIdx.x] = info;
   }
 }
 
@@ -161,19 +185,15 @@ __device__ __forceinline__ void small_scatter_body(const Key& key, const Sink& s
   int* cnt = reinterpret_cast<int*>(stage + kSmallTile);
   int* start = cnt + nbins * kPartThreads;
   const long long base = (long long)blockIdx.x * kSmallTile;
-  // a full tile whose 4096 items all share one bin (the histogram says so:
-  // block mappings, the common case) is a straight copy of consecutive
-  // indices -- no key is evaluated or read at all
-  __shared__ int s_only;
-  if (threadIdx.x == 0) s_only = -1;
-  __syncthreads();
-  if (blockIdx.x + 1 < ntiles && threadIdx.x < nbins) {
-    const long long q = (long long)threadIdx.x * ntiles + blockIdx.x;
-    if (pos0[q + 1] - pos0[q] == kSmallTile) s_only = threadIdx.x;
-  }
-  __syncthreads();
-  if (s_only >= 0) {
-    const int only = s_only;
+  // The histogram pass left a summary of every tile (tile_info): a tile with no
+  // output at all (every key -1: e.g. interior cells of a halo launch) is
+  // skipped; a full tile whose 4096 items all share one bin (block mappings,
+  // the common case) is a straight copy of consecutive indices -- in neither
+  // case is a key evaluated or read.
+  const int info = __ldg(tile_info_of(pos0, nbins, ntiles) + blockIdx.x);
+  if (info == kTileEmpty) return;
+  if (info >= 0) {
+    const int only = info;
     const long long p0 = pos0[(long long)only * ntiles + blockIdx.x];
     key.uniform(base, kSmallTile, only);
     sink.put_run(only, p0, base, kSmallTile);

@@ -123,10 +123,17 @@ using pmdev::kIPT;
 using pmdev::kSmallBins;
 using pmdev::kSmallTile;
 
+// scratch: hist[nbins][ntiles] int64 | tile_info[ntiles] int32 (256-aligned) | scan temp
+inline size_t small_info_bytes(long long ntiles) {
+  return (size_t)((ntiles * 4 + 255) / 256 * 256);
+}
+inline size_t small_scan_offset(long long ntiles, int nbins) {
+  return (size_t)(ntiles * nbins * 8) + small_info_bytes(ntiles);
+}
 inline size_t small_scratch_bytes(long long n, int nbins) {
   const long long ntiles = (n + kSmallTile - 1) / kSmallTile;
   const long long len = ntiles * nbins;
-  return (size_t)(len * 8) + scan_scratch_bytes(len) + 256;
+  return small_scan_offset(ntiles, nbins) + scan_scratch_bytes(len) + 256;
 }
 
 template <class Key>
@@ -163,7 +170,7 @@ int stable_partition_small(Key key, Sink sink, bool scatter, long long n, int nb
   if (ntiles > 0x7FFFFFFFLL) return set_error("partition: too many tiles"), PM_ERR_UNSUPPORTED;
   const long long len = ntiles * nbins;
   long long* hist = reinterpret_cast<long long*>(scratch);
-  void* scan_tmp = reinterpret_cast<char*>(scratch) + len * 8;
+  void* scan_tmp = reinterpret_cast<char*>(scratch) + small_scan_offset(ntiles, nbins);
   const size_t smem_h = small_hist_smem(nbins), smem_s = small_scatter_smem(nbins);
   if (smem_h > 48 * 1024)
     PM_CUDA_TRY(cudaFuncSetAttribute(k_small_hist<Key>,
@@ -183,6 +190,28 @@ int stable_partition_small(Key key, Sink sink, bool scatter, long long n, int nb
                                                                              nbins, ntiles, hist);
     PM_CUDA_TRY(cudaGetLastError());
   }
+  return PM_OK;
+}
+
+// The scatter pass alone, reusing the scanned histogram and tile summary a
+// previous counting call (`scatter` false, same key / n / nbins) left in scratch.
+template <class Key, class Sink>
+int stable_partition_small_scatter(Key key, Sink sink, long long n, int nbins, void* scratch,
+                                   size_t scratch_bytes, cudaStream_t s) {
+  if (nbins < 1 || nbins > kSmallBins)
+    return set_error("partition: scatter-only pass needs 1..%d bins", kSmallBins),
+           PM_ERR_UNSUPPORTED;
+  if (n <= 0) return PM_OK;
+  if (scratch_bytes < small_scratch_bytes(n, nbins))
+    return set_error("partition: scratch too small"), PM_ERR_INVALID;
+  const long long ntiles = (n + kSmallTile - 1) / kSmallTile;
+  const size_t smem_s = small_scatter_smem(nbins);
+  if (smem_s > 48 * 1024)
+    PM_CUDA_TRY(cudaFuncSetAttribute(k_small_scatter<Key, Sink>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
+  k_small_scatter<Key, Sink><<<(unsigned)ntiles, kPartThreads, smem_s, s>>>(
+      key, sink, n, nbins, ntiles, reinterpret_cast<const long long*>(scratch));
+  PM_CUDA_TRY(cudaGetLastError());
   return PM_OK;
 }
 

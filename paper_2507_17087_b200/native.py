@@ -52,6 +52,12 @@ SIGNATURES = {
     "pm_halo_scratch_bytes": (_SZ, [ctypes.POINTER(_I64), _I32, _I32]),
     "pm_halo_lists": (ctypes.c_int, [_VP, ctypes.POINTER(_I64), _I32, ctypes.POINTER(_I32),
                                      _I32, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
+    "pm_halo_tile_scratch_bytes": (ctypes.c_size_t, [ctypes.POINTER(_I64), _I32]),
+    "pm_halo_count": (ctypes.c_int, [_VP, ctypes.POINTER(_I64), _I32, ctypes.POINTER(_I32),
+                                     _I32, _VP, _VP, _SZ, _VP]),
+    "pm_halo_compact": (ctypes.c_int, [_VP, ctypes.POINTER(_I64), _I32, ctypes.POINTER(_I32),
+                                       _I32, _VP, _VP, _VP, _VP]),
+    "pm_halo_gather": (ctypes.c_int, [_VP, _VP, _I64, _I32, _VP, _VP, _VP]),
     "pm_gemm_bf16": (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _I32,
                                     _I32, _VP]),
     "pm_ipc_handle": (ctypes.c_int, [_VP, _VP, ctypes.POINTER(_I64)]),

@@ -6,7 +6,9 @@ every ordered processor pair (src, dst), the cells src must send to dst for
 a halo of width h_n along each dimension.  For block partitions the totals
 equal the reference's ground-truth count `oracle_boundary_count`
 (reference: commvol.py:136-168) and `surface_volume` (commvol.py:94-96) for
-h = 1; tests/test_gpu_halo.py holds the kernel to both.
+h = 1; tests/test_gpu_halo.py holds the kernel to both.  Built by compaction:
+count entries per tile, compact them in slot order, group them by pair with
+K2 (csrc/halo.cu).
 """
 
 from __future__ import annotations
@@ -15,6 +17,7 @@ import ctypes
 from dataclasses import dataclass
 
 from . import native
+from .ownership import partition
 
 
 @dataclass
@@ -52,26 +55,29 @@ def halo_lists(owner, extents, halo, nprocs: int, *, counts_only: bool = False,
     lib = native.lib()
     pairs = nprocs * nprocs
     counts = torch.empty(pairs, dtype=torch.int64, device=dev)
-    offsets = torch.empty(pairs, dtype=torch.int64, device=dev)
-    nbytes = lib.pm_halo_scratch_bytes(ext_c, rank, nprocs)
-    scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    cells = dims = None
+    tbytes = lib.pm_halo_tile_scratch_bytes(ext_c, rank)
+    tiles = torch.empty(tbytes, dtype=torch.uint8, device=dev)
     with torch.cuda.device(dev):
         s = native.stream_ptr(stream)
-        if not counts_only:
-            # size the output from a counting pass first
-            native.check(lib.pm_halo_lists(owner.data_ptr(), ext_c, rank, halo_c, nprocs,
-                                           counts.data_ptr(), offsets.data_ptr(), None, None,
-                                           scratch.data_ptr(), nbytes, s), "pm_halo_lists")
-            total = int(counts.sum())
-            cells = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
-            dims = torch.empty(max(total, 1), dtype=torch.int8, device=dev)
-        native.check(lib.pm_halo_lists(owner.data_ptr(), ext_c, rank, halo_c, nprocs,
-                                       counts.data_ptr(), offsets.data_ptr(),
-                                       None if counts_only else cells.data_ptr(),
-                                       None if counts_only else dims.data_ptr(),
-                                       scratch.data_ptr(), nbytes, s), "pm_halo_lists")
-    if not counts_only:
+        # 1. per-tile entry counts (-> output offsets) and per-pair totals
+        native.check(lib.pm_halo_count(owner.data_ptr(), ext_c, rank, halo_c, nprocs,
+                                       counts.data_ptr(), tiles.data_ptr(), tbytes, s),
+                     "pm_halo_count")
+        if counts_only:
+            offsets = torch.cumsum(counts, 0) - counts
+            return TransferLists(nprocs, counts, offsets, None, None)
         total = int(counts.sum())
-        cells, dims = cells[:total], dims[:total]
-    return TransferLists(nprocs, counts, offsets, cells, dims)
+        # 2. compaction of the entries in slot order
+        keys = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        slots = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
+        native.check(lib.pm_halo_compact(owner.data_ptr(), ext_c, rank, halo_c, nprocs,
+                                         tiles.data_ptr(), keys.data_ptr(), slots.data_ptr(), s),
+                     "pm_halo_compact")
+        # 3. stable grouping by (src, dst) pair (K2) and the (cell, dim) lists
+        own = partition(keys[:total], pairs, stream=stream, check=False)
+        cells = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
+        dims = torch.empty(max(total, 1), dtype=torch.int8, device=dev)
+        native.check(lib.pm_halo_gather(own.perm.data_ptr() if total else None,
+                                        slots.data_ptr(), total, rank, cells.data_ptr(),
+                                        dims.data_ptr(), s), "pm_halo_gather")
+    return TransferLists(nprocs, own.counts, own.offsets, cells[:total], dims[:total])

@@ -79,3 +79,38 @@ def test_stencil_32768_counts(cuda):
     tl = halo_lists(ids, ext, (1, 1), 8, counts_only=True)
     g = cv.BlockGrid(ext, (2, 4))
     assert tl.total == cv.oracle_boundary_count(g, (1, 1), cap=1 << 40) == 262144
+
+
+@pytest.mark.parametrize("ext,halo,P", [((37, 53), (1, 1), 4), ((64, 48), (2, 1), 3),
+                                        ((9, 10, 11), (1, 2, 1), 5), ((200,), (3,), 8),
+                                        ((33, 40), (1, 1), 12)])
+def test_single_call_abi_matches_compaction(cuda, ext, halo, P):
+    """pm_halo_lists (one call, partition of all slots) == the compaction path."""
+    import ctypes
+
+    from paper_2507_17087_b200 import native
+
+    torch = cuda
+    g = torch.Generator(device="cuda").manual_seed(sum(ext) + P)
+    n = 1
+    for e in ext:
+        n *= e
+    owner = torch.randint(0, P, (n,), device="cuda", dtype=torch.int32, generator=g)
+    want = halo_lists(owner, ext, halo, P)
+    lib = native.lib()
+    r = len(ext)
+    ext_c = (ctypes.c_int64 * r)(*ext)
+    halo_c = (ctypes.c_int32 * r)(*halo)
+    counts = torch.empty(P * P, dtype=torch.int64, device="cuda")
+    offsets = torch.empty(P * P, dtype=torch.int64, device="cuda")
+    nb = lib.pm_halo_scratch_bytes(ext_c, r, P)
+    scratch = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    total = want.total
+    cells = torch.empty(max(total, 1), dtype=torch.int64, device="cuda")
+    dims = torch.empty(max(total, 1), dtype=torch.int8, device="cuda")
+    native.check(lib.pm_halo_lists(owner.data_ptr(), ext_c, r, halo_c, P, counts.data_ptr(),
+                                   offsets.data_ptr(), cells.data_ptr(), dims.data_ptr(),
+                                   scratch.data_ptr(), nb, None), "pm_halo_lists")
+    assert torch.equal(counts, want.pair_counts)
+    assert torch.equal(offsets, want.pair_offsets)
+    assert torch.equal(cells[:total], want.cells) and torch.equal(dims[:total], want.dims)
