@@ -352,7 +352,7 @@ pm_map_hist(const int* pts, long long n, long long first, int nbins, long long n
   pmdev::small_hist_body(key, n, nbins, ntiles, hist, smem_words);
 }
 
-extern "C" __global__ void __launch_bounds__(256)
+extern "C" __global__ void __launch_bounds__(256, 6)
 pm_map_scatter(const int* pts, long long n, long long first, int nbins, long long ntiles,
                const long long* __restrict__ pos0, unsigned long long* status, int* out,
                int* perm, long long base) {
@@ -361,7 +361,7 @@ pm_map_scatter(const int* pts, long long n, long long first, int nbins, long lon
   pmdev::small_scatter_body(key, PmPermSink{perm, base}, n, nbins, ntiles, pos0, smem_words);
 }
 
-extern "C" __global__ void __launch_bounds__(256)
+extern "C" __global__ void __launch_bounds__(256, 6)
 pm_map_scatter_peer(const int* pts, long long n, long long first, int nbins, long long ntiles,
                     const long long* __restrict__ pos0, unsigned long long* status, int* out,
                     const long long* tab, long long base) {

@@ -143,8 +143,9 @@ k_small_hist(Key key, long long n, int nbins, long long ntiles, long long* __res
   pmdev::small_hist_body(key, n, nbins, ntiles, hist, smem_words);
 }
 
+// (min 6 CTAs / SM: the uniform-tile copy is a pure store stream, occupancy-bound)
 template <class Key, class Sink>
-__global__ void __launch_bounds__(kPartThreads)
+__global__ void __launch_bounds__(kPartThreads, 6)
 k_small_scatter(Key key, Sink sink, long long n, int nbins, long long ntiles,
                 const long long* __restrict__ pos0) {
   extern __shared__ __align__(16) int smem_words[];
