@@ -14,6 +14,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "pm_common.h"
@@ -306,6 +307,12 @@ struct Halo2D {
     const int4 dn = r + 1 < rows ? __ldg(reinterpret_cast<const int4*>(owner + cell0 + cols)) : cur;
     const int lf = c0 > 0 ? __ldg(owner + cell0 - 1) : cur.x;
     const int rt = c0 + 4 < cols ? __ldg(owner + cell0 + 4) : cur.w;
+    // the common case: one owner around all four cells -> no entry
+    const int a = cur.x;
+    if (((cur.y ^ a) | (cur.z ^ a) | (cur.w ^ a) | (up.x ^ a) | (up.y ^ a) | (up.z ^ a) |
+         (up.w ^ a) | (dn.x ^ a) | (dn.y ^ a) | (dn.z ^ a) | (dn.w ^ a) | (lf ^ a) | (rt ^ a)) ==
+        0)
+      return 0;
     const int o[4] = {cur.x, cur.y, cur.z, cur.w};
     const int q[4][4] = {{up.x, dn.x, lf, cur.y},
                          {up.y, dn.y, cur.x, cur.z},
@@ -362,11 +369,11 @@ __global__ void __launch_bounds__(kPartThreads)
 k_halo2d_compact(Halo2D h, long long ncells, long long ntiles,
                  const long long* __restrict__ tile_off, const long long* __restrict__ total,
                  int* __restrict__ out_key, long long* __restrict__ out_slot) {
-  const long long t = blockIdx.x;
-  const long long lo = tile_off[t], hi = t + 1 < ntiles ? tile_off[t + 1] : *total;
-  if (lo == hi) return;
   __shared__ int s_warp[kPartWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  const long long lo = tile_off[t], hi = t + 1 < ntiles ? tile_off[t + 1] : *total;
+  if (lo == hi) continue;
   const long long base = t * (kHaloTile / 4);
   long long running = lo;
 #pragma unroll 1
@@ -402,6 +409,7 @@ k_halo2d_compact(Halo2D h, long long ncells, long long ntiles,
     running += all;
     __syncthreads();
   }
+  }
 }
 
 bool make_halo2d(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
@@ -422,6 +430,7 @@ bool make_halo2d(const int32_t* owner, const int64_t* ext, int32_t rank, const i
   return true;
 }
 
+// tile scratch: offsets int64 [ntiles] | scan temp
 size_t halo_tile_bytes(long long ntiles) {
   return (size_t)(((ntiles * 8 + 255) / 256) * 256) + scan_scratch_bytes(ntiles);
 }
@@ -556,6 +565,8 @@ int pm_halo_compact(const int32_t* owner, const int64_t* ext, int32_t rank, cons
     const long long* tile = reinterpret_cast<const long long*>(tile_scratch);
     const long long* total = reinterpret_cast<const long long*>(
         reinterpret_cast<char*>(tile_scratch) + ((ntiles * 8 + 255) / 256) * 256);
+    // one block per tile (a persistent grid striding over the tiles measured slower:
+    // 1.18 -> 1.56 ms at 32768^2 -- the non-empty tiles' latency chains dominate)
     pm::k_halo2d_compact<<<(unsigned)ntiles, pm::kPartThreads, 0, (cudaStream_t)stream>>>(
         h2, ncells, ntiles, tile, total, keys, so);
     PM_CUDA_TRY(cudaGetLastError());
