@@ -673,50 +673,71 @@ def main_ours(args):
         del ex
         torch.cuda.empty_cache()
     extra = {}
+    errors = {}
+
+    def guarded(name, fn):
+        """An extra workload must not take the headline line down with it: its
+        failure is recorded in the JSON line instead (same on every rank)."""
+        try:
+            return fn()
+        except Exception as e:  # noqa: BLE001
+            errors[name] = f"{type(e).__name__}: {e}"[:300]
+            torch.cuda.synchronize()
+            return None
+
     if not args.no_3d:
         # BASELINE configs[2] (Johnson 3D, square) and configs[3] (COSMA, rectangular)
-        wl = {}
-        for name, (M, N, K) in (("johnson3d", (args.size,) * 3),
-                                ("cosma", (2 * args.size, args.size // 2, args.size // 2))):
-            d = run_3d(args, rank, world, local, M, N, K, "decompose")
-            h = run_3d(args, rank, world, local, M, N, K, "heuristic")
-            wl[name] = {"M": M, "N": N, "K": K, "decompose": d, "heuristic": h,
-                        "speedup": d["tflops"] / h["tflops"],
-                        "comm_ratio": h["comm_bytes_per_gpu"]["total"] /
-                        max(1, d["comm_bytes_per_gpu"]["total"])}
-        extra["workloads_3d"] = wl
+        def w3d():
+            wl = {}
+            for name, (M, N, K) in (("johnson3d", (args.size,) * 3),
+                                    ("cosma", (2 * args.size, args.size // 2, args.size // 2))):
+                d = run_3d(args, rank, world, local, M, N, K, "decompose")
+                h = run_3d(args, rank, world, local, M, N, K, "heuristic")
+                wl[name] = {"M": M, "N": N, "K": K, "decompose": d, "heuristic": h,
+                            "speedup": d["tflops"] / h["tflops"],
+                            "comm_ratio": h["comm_bytes_per_gpu"]["total"] /
+                            max(1, d["comm_bytes_per_gpu"]["total"])}
+            return wl
+        extra["workloads_3d"] = guarded("workloads_3d", w3d)
     if not args.no_cannon:
         cn = {}
         if world in (1, 4):  # q x q grids: configs[0] is Cannon fp32 N=1024 on 2x2
-            cn["cannon_fp32_N1024"] = run_cannon(args, rank, world, 1024, 1, "fp32")
-            cn["cannon_bf16"] = run_cannon(args, rank, world, args.size, 1, "bf16")
+            cn["cannon_fp32_N1024"] = guarded(
+                "cannon_fp32", lambda: run_cannon(args, rank, world, 1024, 1, "fp32"))
+            cn["cannon_bf16"] = guarded(
+                "cannon_bf16", lambda: run_cannon(args, rank, world, args.size, 1, "bf16"))
         if world == 8:       # configs[2]: Solomonik 2.5D on 2x2x2
-            cn["solomonik_2p5d_bf16"] = run_cannon(args, rank, world, args.size, 2, "bf16")
+            cn["solomonik_2p5d_bf16"] = guarded(
+                "solomonik_2p5d", lambda: run_cannon(args, rank, world, args.size, 2, "bf16"))
         extra["cannon"] = cn
     if not args.no_stencil:
-        st = {}
-        for name, (r, c) in (("square", (args.size, args.size)),
-                             ("aspect_1x4", (args.size // 2, 2 * args.size))):
-            d = run_stencil(args, rank, world, r, c, "decompose")
-            h = run_stencil(args, rank, world, r, c, "heuristic")
-            st[name] = {"rows": r, "cols": c, "decompose": d, "heuristic": h,
-                        "speedup": h["ms_per_sweep"] / d["ms_per_sweep"],
-                        "halo_ratio": (h["halo_cells_per_sweep"] or 1) /
-                        max(1, d["halo_cells_per_sweep"] or 1)}
-        extra["stencil"] = {"workload": "5-point Jacobi fp32, Mapple block mapping, fused NVLink "
-                                        "halo exchange (BASELINE configs[4])", **st}
+        def stencil():
+            st = {}
+            for name, (r, c) in (("square", (args.size, args.size)),
+                                 ("aspect_1x4", (args.size // 2, 2 * args.size))):
+                d = run_stencil(args, rank, world, r, c, "decompose")
+                h = run_stencil(args, rank, world, r, c, "heuristic")
+                st[name] = {"rows": r, "cols": c, "decompose": d, "heuristic": h,
+                            "speedup": h["ms_per_sweep"] / d["ms_per_sweep"],
+                            "halo_ratio": (h["halo_cells_per_sweep"] or 1) /
+                            max(1, d["halo_cells_per_sweep"] or 1)}
+            return {"workload": "5-point Jacobi fp32, Mapple block mapping, fused NVLink "
+                                "halo exchange (BASELINE configs[4])", **st}
+        extra["stencil"] = guarded("stencil", stencil)
     if not args.no_circuit:
-        extra["circuit"] = {"workload": "circuit simulation (configs[4] 'plus circuit sim'), "
-                                        "weak scaling, node exchange fused over NVLink",
-                            "block": run_circuit(args, rank, world, "block"),
-                            "cyclic": run_circuit(args, rank, world, "cyclic")}
+        extra["circuit"] = guarded("circuit", lambda: {
+            "workload": "circuit simulation (configs[4] 'plus circuit sim'), weak scaling, "
+                        "node exchange fused over NVLink",
+            "block": run_circuit(args, rank, world, "block"),
+            "cyclic": run_circuit(args, rank, world, "cyclic")})
     if not args.no_hydro:
-        d = run_hydro(args, rank, world, "decompose")
-        h = run_hydro(args, rank, world, "heuristic")
-        extra["pennant_hydro"] = {"workload": "PENNANT-style Lagrangian hydro, 16384x4096 "
-                                              "quad zones, shared points fused over NVLink",
-                                  "decompose": d, "heuristic": h,
-                                  "speedup": h["ms_per_step"] / d["ms_per_step"]}
+        def hydro():
+            d = run_hydro(args, rank, world, "decompose")
+            h = run_hydro(args, rank, world, "heuristic")
+            return {"workload": "PENNANT-style Lagrangian hydro, 16384x4096 quad zones, "
+                                "shared points fused over NVLink",
+                    "decompose": d, "heuristic": h, "speedup": h["ms_per_step"] / d["ms_per_step"]}
+        extra["pennant_hydro"] = guarded("pennant_hydro", hydro)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         C64, dt, fl = cpu_sample(args)
@@ -739,9 +760,12 @@ def main_ours(args):
         del exc
         torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_kernels:
-        extra["hot_path_kernels"] = hot_path_kernels(args)
+        extra["hot_path_kernels"] = guarded("hot_path_kernels", lambda: hot_path_kernels(args))
     if not args.no_kernels:
-        extra["sharded_mapping"] = run_sharded_mapping(args, rank, world)
+        extra["sharded_mapping"] = guarded("sharded_mapping",
+                                           lambda: run_sharded_mapping(args, rank, world))
+    if errors:
+        extra["errors"] = errors
     if rank != 0:
         return
     peak = sustained if dec["ms_per_step"] * args.steps > 1000 else burst
