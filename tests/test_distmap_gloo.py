@@ -83,7 +83,7 @@ def _free_port():
     return port
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_sharded_ownership_matches_shard_tree(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

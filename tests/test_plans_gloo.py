@@ -122,7 +122,7 @@ def _free_port():
     return port
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_plans_agree_across_ranks(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
