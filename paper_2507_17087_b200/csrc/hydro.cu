@@ -94,8 +94,44 @@ k_hydro_points(const __grid_constant__ HydroArgs a) {
   float *px = v.px[me], *py = v.py[me], *ux = v.ux[me], *uy = v.uy[me];
   float2* f = reinterpret_cast<float2*>(v.fxy[me]);
   const float dt = v.dt;
-  for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < v.n_points;
-       n += (long long)gridDim.x * blockDim.x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // four points per thread: 16-byte loads / stores of every array (all base
+  // pointers are 16-byte aligned allocations; the tail goes point by point)
+  const long long nv = v.n_points >> 2;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < nv; g += stride) {
+    const float4 m4 = __ldg(reinterpret_cast<const float4*>(v.pm) + g);
+    const char4 b4 = __ldg(reinterpret_cast<const char4*>(v.pbc) + g);
+    const float4 fa = reinterpret_cast<const float4*>(f)[2 * g];      // fx0 fy0 fx1 fy1
+    const float4 fb = reinterpret_cast<const float4*>(f)[2 * g + 1];  // fx2 fy2 fx3 fy3
+    float4 u = reinterpret_cast<float4*>(ux)[g], w = reinterpret_cast<float4*>(uy)[g];
+    float4 x = reinterpret_cast<float4*>(px)[g], y = reinterpret_cast<float4*>(py)[g];
+    const float fxs[4] = {fa.x, fa.z, fb.x, fb.z}, fys[4] = {fa.y, fa.w, fb.y, fb.w};
+    const float ms[4] = {m4.x, m4.y, m4.z, m4.w};
+    const int bcs[4] = {b4.x, b4.y, b4.z, b4.w};
+    float* uu = &u.x;
+    float* ww = &w.x;
+    float* xx = &x.x;
+    float* yy = &y.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float rm = 1.0f / ms[j];
+      const float ax = (bcs[j] & 1) ? 0.f : fxs[j] * rm;
+      const float ay = (bcs[j] & 2) ? 0.f : fys[j] * rm;
+      const float u1 = uu[j] + dt * ax, w1 = ww[j] + dt * ay;
+      xx[j] += dt * 0.5f * (uu[j] + u1);
+      yy[j] += dt * 0.5f * (ww[j] + w1);
+      uu[j] = u1;
+      ww[j] = w1;
+    }
+    reinterpret_cast<float4*>(ux)[g] = u;
+    reinterpret_cast<float4*>(uy)[g] = w;
+    reinterpret_cast<float4*>(px)[g] = x;
+    reinterpret_cast<float4*>(py)[g] = y;
+    reinterpret_cast<float4*>(f)[2 * g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    reinterpret_cast<float4*>(f)[2 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (long long n = 4 * nv + (long long)blockIdx.x * blockDim.x + threadIdx.x; n < v.n_points;
+       n += stride) {
     const float rm = 1.0f / v.pm[n];
     const int bc = v.pbc[n];
     const float2 fn = f[n];
@@ -130,7 +166,7 @@ int pm_hydro_step(const pm_hydro_view* view, int32_t phase, void* stream) {
     pm::k_hydro_zones<<<(unsigned)((view->n_zones + 255) / 256), 256, 0, s>>>(a);
   } else if (phase == 1) {
     if (view->n_points == 0) return PM_OK;
-    long long blocks = (view->n_points + 255) / 256;
+    long long blocks = (view->n_points / 4 + 255) / 256 + 1;
     const long long cap = (long long)pm::num_sms() * 8;
     if (blocks > cap) blocks = cap;
     pm::k_hydro_points<<<(unsigned)blocks, 256, 0, s>>>(a);
