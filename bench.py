@@ -271,6 +271,9 @@ def run_cannon(args, rank, world, N, layers, dtype):
 
     from paper_2507_17087_b200.executors.cannon import MappedCannon, cannon_moves
 
+    # (CUDA-graph replay of the whole multiply is supported -- MappedCannon(graph=True) --
+    # but measured slower at configs[0] on 4 GPUs: 0.35 vs 0.14 ms, the captured NCCL
+    # barriers dominate; the eager path is timed)
     ex = MappedCannon(N, layers=layers, rank=rank, world=world, dtype=dtype, seed=31)
     cs = torch.cuda.current_stream()
     for _ in range(args.warmup):

@@ -31,11 +31,13 @@ def main():
         if world % c == 0 and isqrt(world // c) ** 2 * c == world and isqrt(world // c) % c == 0:
             configs.append(c)
     for c in configs:
-        for dtype, N in (("fp32", 1024), ("bf16", 2048)):
+        for dtype, N, graph in (("fp32", 1024, False), ("fp32", 1024, True), ("bf16", 2048, False),
+                                ("bf16", 2048, True)):
             if dtype == "fp32" and c > 1:
                 continue
-            ex = MappedCannon(N, layers=c, rank=rank, world=world, dtype=dtype, seed=21)
-            for _ in range(2):
+            ex = MappedCannon(N, layers=c, rank=rank, world=world, dtype=dtype, seed=21,
+                              graph=graph)
+            for _ in range(5):  # eager warm-up per buffer, then graph capture + replays
                 ex.step()
             C = ex.result()
             torch.cuda.synchronize()
@@ -58,7 +60,7 @@ def main():
             want = O.map_launch(parse(HIER_MAPPERS), task, ("GPU", *ex.machine), ispace)
             got = [ex.owner[(a, b, 0)] for a in range(q) for b in range(q)] if c == 1 else \
                 [ex.owner[(a, b, d)] for a in range(q) for b in range(q) for d in range(c)]
-            out.append({"c": c, "dtype": dtype, "N": N, "rank": rank, "err": err,
+            out.append({"c": c, "dtype": dtype, "N": N, "graph": graph, "rank": rank, "err": err,
                         "moves": sum(moves), "want_moves": cannon_moves(q, c),
                         "owners_ok": got == want})
             if world > 1:
