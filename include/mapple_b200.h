@@ -229,7 +229,7 @@ typedef struct pm_stencil_view {
   int32_t* my_flags;         /* [world] sweep-done flags pushed by neighbours  */
   int32_t* nbr_flag_slot[4]; /* &neighbour.my_flags[my rank] (peer pointers)   */
   int32_t nbr_rank[4];
-  uint32_t* ticket;          /* cumulative CTA ticket (device, zero at start)  */
+  uint32_t* ticket;          /* unused (kept for the struct layout)           */
 } pm_stencil_view;
 int pm_stencil_sweep(const pm_stencil_view* view, int32_t sweep, void* stream);
 

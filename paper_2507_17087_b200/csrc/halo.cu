@@ -285,33 +285,40 @@ __global__ void k_halo_gather(const int* __restrict__ perm, const long long* __r
   }
 }
 
-// ---- 2-D, h = (1, 1), cols % 4 == 0: four cells per thread from int4 loads ------------
+// ---- 2-D, h = (1, 1), cols % 4 == 0: column strips with a rolling row window -------
 //
-// The common stencil case.  A thread takes 4 consecutive cells of one row (16-byte
-// loads of the row and of the rows above and below, two scalar loads for the left
-// and right ends) and derives the 16 slots' keys in registers; most groups have no
-// entry at all and cost one comparison.  Tiles are the same 8192 slots (2048 cells,
-// 2 groups per thread) as the generic kernels, so the scan is shared.
-struct Halo2D {
+// The common stencil case.  A block owns a strip of kStripCells columns (4 cells per
+// thread, one 16-byte load per row) and walks kStripRows rows down it, keeping the
+// rows above and below in registers, so every owner is read from HBM once (plus one
+// halo row per strip); the left / right neighbours come from the adjacent lanes by
+// shuffle.  Most 4-cell groups have no entry at all and cost one comparison.  A tile
+// is one row segment of the strip, tile index row * nseg + seg (row-major = slot
+// order); the compaction revisits only strips holding entries.
+constexpr int kStripCells = 4 * kPartThreads;  // 1024 columns per strip
+constexpr int kStripRows = 64;                 // rows per block (one mask bit each)
+#ifndef PM_STRIP_BATCH
+#define PM_STRIP_BATCH 4
+#endif
+#ifndef PM_STRIP_MINB
+#define PM_STRIP_MINB 4
+#endif
+constexpr int kStripBatch = PM_STRIP_BATCH;    // rows of loads in flight per thread
+
+struct Strip2D {
   const int* __restrict__ owner;
-  unsigned rows, cols, div_m, div_s;
+  long long rows, cols;
+  int nseg;
   int nprocs;
-  // keys of the 16 slots of the 4 cells starting at cell0 (slot order: cell, dd);
-  // returns the number of entries
-  __device__ __forceinline__ int keys(unsigned cell0, int (&k)[16]) const {
-    const unsigned t = __umulhi(div_m, cell0);
-    const unsigned r = (t + ((cell0 - t) >> 1)) >> div_s;
-    const unsigned c0 = cell0 - r * cols;
-    const int4 cur = __ldg(reinterpret_cast<const int4*>(owner + cell0));
-    const int4 up = r > 0 ? __ldg(reinterpret_cast<const int4*>(owner + cell0 - cols)) : cur;
-    const int4 dn = r + 1 < rows ? __ldg(reinterpret_cast<const int4*>(owner + cell0 + cols)) : cur;
-    const int lf = c0 > 0 ? __ldg(owner + cell0 - 1) : cur.x;
-    const int rt = c0 + 4 < cols ? __ldg(owner + cell0 + 4) : cur.w;
-    // the common case: one owner around all four cells -> no entry
+
+  __device__ __forceinline__ int4 row(long long r, long long c0) const {
+    return __ldg(reinterpret_cast<const int4*>(owner + r * cols + c0));
+  }
+  // keys of the 16 slots (cell, dd) of the 4 cells cur; returns the number of entries
+  __device__ __forceinline__ int keys(const int4& up, const int4& cur, const int4& dn, int lf,
+                                      int rt, int (&k)[16]) const {
     const int a = cur.x;
     if (((cur.y ^ a) | (cur.z ^ a) | (cur.w ^ a) | (up.x ^ a) | (up.y ^ a) | (up.z ^ a) |
-         (up.w ^ a) | (dn.x ^ a) | (dn.y ^ a) | (dn.z ^ a) | (dn.w ^ a) | (lf ^ a) | (rt ^ a)) ==
-        0)
+         (up.w ^ a) | (dn.x ^ a) | (dn.y ^ a) | (dn.z ^ a) | (dn.w ^ a) | (lf ^ a) | (rt ^ a)) == 0)
       return 0;
     const int o[4] = {cur.x, cur.y, cur.z, cur.w};
     const int q[4][4] = {{up.x, dn.x, lf, cur.y},
@@ -333,106 +340,215 @@ struct Halo2D {
   }
 };
 
-__global__ void __launch_bounds__(kPartThreads)
-k_halo2d_count(Halo2D h, long long ncells, int npairs, long long* __restrict__ tile_cnt,
-               unsigned long long* __restrict__ pair_cnt) {
-  extern __shared__ int sp[];
-  __shared__ int s_tot;
-  for (int b = threadIdx.x; b < npairs; b += kPartThreads) sp[b] = 0;
-  if (threadIdx.x == 0) s_tot = 0;
-  __syncthreads();
-  const long long base = (long long)blockIdx.x * (kHaloTile / 4);
-  int c = 0;
+// Walks the block's rows; calls f(i, up, cur, dn, lf, rt) for row r0 + i, i < nr.
+// Lanes past the last column re-read the last group (the caller masks them with
+// `active`); the column left of column 0 is column 0 itself and the column right of
+// the last is the last (= no entry).  Blocks touching the first or last grid row
+// (kClamp) also clamp row indices: the row above row 0 is row 0, the row below the
+// last row the last row.  All lanes of every warp call f.
+template <bool kClamp, class F>
+__device__ __forceinline__ void strip_walk(const Strip2D& h, long long r0, int nr, long long c0,
+                                           F&& f) {
+  const int lane = threadIdx.x & 31;
+  const long long cc = c0 < h.cols ? c0 : h.cols - 4;
+  const bool has_rt = c0 + 4 < h.cols;
+  const int* col = h.owner + cc;
+  const int* edge = h.owner + (lane == 0 ? (cc > 0 ? cc - 1 : 0) : min(cc + 4, h.cols - 1));
+  const bool edge_lane = lane == 0 || lane == 31;
+  const size_t st = (size_t)h.cols;
+  const unsigned last = (unsigned)(h.rows - 1), ur0 = (unsigned)r0;
+  int4 cur = __ldg(reinterpret_cast<const int4*>(col + (size_t)ur0 * st));
+  int4 up = __ldg(reinterpret_cast<const int4*>(col + (size_t)(ur0 ? ur0 - 1 : 0) * st));
+  const int* pr = col + (size_t)(ur0 + 1) * st;  // row r0 + i + 1 (unclamped walk)
+  const int* pe = edge + (size_t)ur0 * st;       // edge column of row r0 + i
+#pragma unroll 1
+  for (int i = 0; i < nr; i += kStripBatch) {
+    int4 nx[kStripBatch];
+    int ed[kStripBatch];
 #pragma unroll
-  for (int g = 0; g < 2; ++g) {
-    const long long cell0 = base + (long long)(g * kPartThreads + threadIdx.x) * 4;
-    if (cell0 >= ncells) break;
+    for (int u = 0; u < kStripBatch; ++u) {
+      if constexpr (kClamp) {
+        const unsigned r = min(ur0 + i + u, last);
+        nx[u] = __ldg(reinterpret_cast<const int4*>(col + (size_t)min(r + 1, last) * st));
+        ed[u] = edge_lane ? __ldg(edge + (size_t)r * st) : 0;
+      } else {
+        nx[u] = __ldg(reinterpret_cast<const int4*>(pr + u * st));
+        ed[u] = edge_lane ? __ldg(pe + u * st) : 0;
+      }
+    }
+    if constexpr (!kClamp) {
+      pr += kStripBatch * st;
+      pe += kStripBatch * st;
+    }
+#pragma unroll
+    for (int u = 0; u < kStripBatch; ++u) {
+      const int4 dn = nx[u];
+      int lf = __shfl_up_sync(0xffffffffu, cur.w, 1);
+      int rt = __shfl_down_sync(0xffffffffu, cur.x, 1);
+      if (lane == 0) lf = ed[u];
+      if (lane == 31) rt = ed[u];
+      if (!has_rt) rt = cur.w;
+      if (kClamp ? i + u < nr : true) f(i + u, up, cur, dn, lf, rt);  // block-uniform
+      up = cur;
+      cur = dn;
+    }
+  }
+}
+
+// interior row blocks (rows r0 - 1 .. r0 + kStripRows exist) walk unclamped
+template <class F>
+__device__ __forceinline__ void strip_rows(const Strip2D& h, long long r0, int nr, long long c0,
+                                           F&& f) {
+  if (r0 > 0 && r0 + kStripRows < h.rows)
+    strip_walk<false>(h, r0, kStripRows, c0, f);
+  else
+    strip_walk<true>(h, r0, nr, c0, f);
+}
+
+__global__ void __launch_bounds__(kPartThreads, PM_STRIP_MINB)
+k_halo2d_count(Strip2D h, int npairs, long long* __restrict__ tile_cnt,
+               unsigned long long* __restrict__ pair_cnt, unsigned long long* __restrict__ warp_rows,
+               unsigned short* __restrict__ warp_pre) {
+  extern __shared__ int sp[];  // [npairs]
+  __shared__ int s_row[kStripRows][kPartWarps];
+  __shared__ int s_any;
+  for (int b = threadIdx.x; b < npairs; b += kPartThreads) sp[b] = 0;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  const int seg = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long r0 = (long long)blockIdx.y * kStripRows;
+  const int nr = (int)min((long long)kStripRows, h.rows - r0);
+  const long long c0 = (long long)seg * kStripCells + 4 * threadIdx.x;
+  const bool active = c0 < h.cols;
+  bool any = false;
+  strip_rows(h, r0, nr, c0, [&](int i, const int4& up, const int4& cur, const int4& dn, int lf,
+                                int rt) {
     int k[16];
-    const int n = h.keys((unsigned)cell0, k);
+    const int n = active ? h.keys(up, cur, dn, lf, rt, k) : 0;
     if (n) {
-      c += n;
+      any = true;
 #pragma unroll
       for (int s = 0; s < 16; ++s)
         if (k[s] >= 0) atomicAdd(&sp[k[s]], 1);
     }
-  }
-  for (int d = 16; d; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_tot, c);
+    const int tot = __reduce_add_sync(0xffffffffu, n);
+    if (lane == 0) s_row[i][warp] = tot;
+  });
+  if (any) s_any = 1;
   __syncthreads();
-  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = s_tot;
-  if (s_tot)
+  if (threadIdx.x < nr) {
+    int c = 0;
+#pragma unroll
+    for (int w = 0; w < kPartWarps; ++w) c += s_row[threadIdx.x][w];
+    tile_cnt[(r0 + threadIdx.x) * h.nseg + seg] = c;
+  }
+  // per warp: which of the block's rows hold its entries (the compaction skips the
+  // rest) and, in non-empty tiles, its first entry within the tile (<= 4 * kStripCells)
+  unsigned long long rows_hit = 0;
+#pragma unroll
+  for (int q = 0; q < kStripRows / 32; ++q) {
+    const int i = 32 * q + lane;
+    int before = 0, all = 0;
+    if (i < nr) {
+#pragma unroll
+      for (int v = 0; v < kPartWarps; ++v) {
+        const int x = s_row[i][v];
+        before += v < warp ? x : 0;
+        all += x;
+      }
+      if (all) warp_pre[((r0 + i) * h.nseg + seg) * kPartWarps + warp] = (unsigned short)before;
+    }
+    rows_hit |= (unsigned long long)__ballot_sync(0xffffffffu, i < nr && s_row[i < nr ? i : 0][warp]) << (32 * q);
+  }
+  if (lane == 0) warp_rows[((long long)blockIdx.y * h.nseg + seg) * kPartWarps + warp] = rows_hit;
+  if (s_any)
     for (int b = threadIdx.x; b < npairs; b += kPartThreads)
       if (sp[b]) atomicAdd(pair_cnt + b, (unsigned long long)sp[b]);
 }
 
-__global__ void __launch_bounds__(kPartThreads)
-k_halo2d_compact(Halo2D h, long long ncells, long long ntiles,
-                 const long long* __restrict__ tile_off, const long long* __restrict__ total,
-                 int* __restrict__ out_key, long long* __restrict__ out_slot) {
-  __shared__ int s_warp[kPartWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-  const long long lo = tile_off[t], hi = t + 1 < ntiles ? tile_off[t + 1] : *total;
-  if (lo == hi) continue;
-  const long long base = t * (kHaloTile / 4);
-  long long running = lo;
-#pragma unroll 1
-  for (int g = 0; g < 2; ++g) {
-    const long long cell0 = base + (long long)(g * kPartThreads + threadIdx.x) * 4;
+__global__ void __launch_bounds__(kPartThreads, 3)
+k_halo2d_compact(Strip2D h, const long long* __restrict__ tile_off,
+                 const unsigned long long* __restrict__ warp_rows,
+                 const unsigned short* __restrict__ warp_pre, int* __restrict__ out_key,
+                 long long* __restrict__ out_slot) {
+  const int seg = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned long long mine = warp_rows[((long long)blockIdx.y * h.nseg + seg) * kPartWarps + warp];
+  if (!mine) return;  // warp-uniform; no block-wide barrier below
+  const long long r0 = (long long)blockIdx.y * kStripRows;
+  const int nr = (int)min((long long)kStripRows, h.rows - r0);
+  // lane i: first output slot of this warp's entries in rows r0 + i and r0 + 32 + i
+  long long first[2] = {0, 0};
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    if (mine >> (32 * q + lane) & 1) {
+      const long long t = (r0 + 32 * q + lane) * h.nseg + seg;
+      first[q] = tile_off[t] + warp_pre[t * kPartWarps + warp];
+    }
+  const long long c0 = (long long)seg * kStripCells + 4 * threadIdx.x;
+  const bool active = c0 < h.cols;
+  strip_rows(h, r0, nr, c0, [&](int i, const int4& up, const int4& cur, const int4& dn, int lf,
+                                int rt) {
+    const long long row_first = __shfl_sync(0xffffffffu, i < 32 ? first[0] : first[1], i & 31);
+    if (!(mine >> i & 1)) return;  // warp-uniform
     int k[16];
-    const int c = cell0 < ncells ? h.keys((unsigned)cell0, k) : 0;
+    const int c = active ? h.keys(up, cur, dn, lf, rt, k) : 0;
     int incl = c;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int u = __shfl_up_sync(0xffffffffu, incl, d);
       if (lane >= d) incl += u;
     }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    int before = 0, all = 0;
-#pragma unroll
-    for (int w = 0; w < kPartWarps; ++w) {
-      const int v = s_warp[w];
-      before += w < warp ? v : 0;
-      all += v;
-    }
     if (c) {
-      long long pos = running + before + incl - c;
+      long long pos = row_first + incl - c;
+      const long long slot0 = ((r0 + i) * h.cols + c0) * 4;
 #pragma unroll
       for (int s = 0; s < 16; ++s)
         if (k[s] >= 0) {
           out_key[pos] = k[s];
-          out_slot[pos] = cell0 * 4 + s;
+          out_slot[pos] = slot0 + s;
           ++pos;
         }
     }
-    running += all;
-    __syncthreads();
-  }
-  }
+  });
 }
 
-bool make_halo2d(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
-                 int32_t nprocs, Halo2D* h) {
-  if (rank != 2 || halo[0] != 1 || halo[1] != 1 || ext[1] % 4 != 0 || ext[1] < 4 ||
-      (uintptr_t)owner % 16 != 0 || ext[0] * ext[1] * 4 > (1LL << 32) || nprocs < 1 ||
-      nprocs > 64)
+bool make_strip2d(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
+                  int32_t nprocs, Strip2D* h) {
+  if (rank != 2 || halo[0] != 1 || halo[1] != 1 || ext[1] % 4 != 0 || ext[1] < 4 || ext[0] < 1 ||
+      (uintptr_t)owner % 16 != 0 || nprocs < 1 || nprocs > 64)
     return false;
+  const long long nseg = (ext[1] + kStripCells - 1) / kStripCells;
+  if (ext[1] > 0x7FFFFFFF || (ext[0] + kStripRows - 1) / kStripRows > 65535) return false;
   h->owner = owner;
-  h->rows = (unsigned)ext[0];
-  h->cols = (unsigned)ext[1];
+  h->rows = ext[0];
+  h->cols = ext[1];
+  h->nseg = (int)nseg;
   h->nprocs = nprocs;
-  const unsigned long long d = (unsigned long long)ext[1];
-  unsigned l = 0;
-  while ((1ull << l) < d) ++l;
-  h->div_m = (unsigned)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
-  h->div_s = l - 1;
   return true;
 }
 
 // tile scratch: offsets int64 [ntiles] | scan temp
 size_t halo_tile_bytes(long long ntiles) {
   return (size_t)(((ntiles * 8 + 255) / 256) * 256) + scan_scratch_bytes(ntiles);
+}
+
+// strip kernels: tile scratch | per-(row block, strip, warp) row masks |
+// per-(tile, warp) first entry (written for non-empty tiles only)
+inline size_t pad256(size_t b) { return (b + 255) / 256 * 256; }
+size_t strip_mask_bytes(const Strip2D& h) {
+  return pad256((size_t)((h.rows + kStripRows - 1) / kStripRows) * h.nseg * kPartWarps * 8);
+}
+size_t strip_tile_bytes(const Strip2D& h) {
+  return pad256(halo_tile_bytes(h.rows * h.nseg)) + strip_mask_bytes(h) +
+         (size_t)h.rows * h.nseg * kPartWarps * 2;
+}
+unsigned long long* strip_warp_rows(const Strip2D& h, void* scratch) {
+  return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(scratch) +
+                                     pad256(halo_tile_bytes(h.rows * h.nseg)));
+}
+unsigned short* strip_warp_pre(const Strip2D& h, void* scratch) {
+  return reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(strip_warp_rows(h, scratch)) +
+                                           strip_mask_bytes(h));
 }
 
 template <class Key>
@@ -507,8 +623,15 @@ size_t pm_halo_tile_scratch_bytes(const int64_t* ext, int32_t rank) {
   if (!ext || rank < 1 || rank > 3) return 256;
   long long cells = 1;
   for (int m = 0; m < rank; ++m) cells *= ext[m];
-  const long long ntiles = (cells * 2 * rank + pm::kHaloTile - 1) / pm::kHaloTile;
-  return pm::halo_tile_bytes(ntiles);
+  long long ntiles = (cells * 2 * rank + pm::kHaloTile - 1) / pm::kHaloTile;
+  size_t bytes = pm::halo_tile_bytes(ntiles);
+  if (rank == 2 && ext[0] >= 1 && ext[1] >= 4) {  // the strip kernels' layout
+    pm::Strip2D h{};
+    h.rows = ext[0];
+    h.nseg = (int)((ext[1] + pm::kStripCells - 1) / pm::kStripCells);
+    bytes = std::max(bytes, pm::strip_tile_bytes(h));
+  }
+  return bytes;
 }
 
 int pm_halo_count(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
@@ -522,16 +645,18 @@ int pm_halo_count(const int32_t* owner, const int64_t* ext, int32_t rank, const 
            PM_ERR_INVALID;
   const long long items = ncells * 2 * rank;
   auto* pc = reinterpret_cast<long long*>(pair_counts);
-  pm::Halo2D h2;
-  if (pm::make_halo2d(owner, ext, rank, halo, nprocs, &h2)) {
-    const long long ntiles = (items + pm::kHaloTile - 1) / pm::kHaloTile;
-    if (bytes < pm::halo_tile_bytes(ntiles))
+  pm::Strip2D h2;
+  if (pm::make_strip2d(owner, ext, rank, halo, nprocs, &h2)) {
+    const long long ntiles = h2.rows * h2.nseg;
+    if (bytes < pm::strip_tile_bytes(h2))
       return pm::set_error("pm_halo_count: scratch too small"), PM_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     PM_CUDA_TRY(cudaMemsetAsync(pc, 0, sizeof(long long) * nprocs * nprocs, s));
     long long* tile = reinterpret_cast<long long*>(tile_scratch);
-    pm::k_halo2d_count<<<(unsigned)ntiles, pm::kPartThreads, sizeof(int) * nprocs * nprocs, s>>>(
-        h2, ncells, nprocs * nprocs, tile, reinterpret_cast<unsigned long long*>(pc));
+    const dim3 grid((unsigned)h2.nseg, (unsigned)((h2.rows + pm::kStripRows - 1) / pm::kStripRows));
+    pm::k_halo2d_count<<<grid, pm::kPartThreads, sizeof(int) * nprocs * nprocs, s>>>(
+        h2, nprocs * nprocs, tile, reinterpret_cast<unsigned long long*>(pc),
+        pm::strip_warp_rows(h2, tile_scratch), pm::strip_warp_pre(h2, tile_scratch));
     PM_CUDA_TRY(cudaGetLastError());
     return pm::exclusive_scan_i64(tile, ntiles,
                                   reinterpret_cast<char*>(tile_scratch) +
@@ -558,17 +683,14 @@ int pm_halo_compact(const int32_t* owner, const int64_t* ext, int32_t rank, cons
     return pm::set_error("pm_halo_compact: bad arguments"), PM_ERR_INVALID;
   const long long items = ncells * 2 * rank;
   auto* so = reinterpret_cast<long long*>(slots);
-  pm::Halo2D h2;
-  if (pm::make_halo2d(owner, ext, rank, halo, nprocs, &h2)) {
-    const long long ntiles = (items + pm::kHaloTile - 1) / pm::kHaloTile;
-    if (ntiles == 0) return PM_OK;
+  pm::Strip2D h2;
+  if (pm::make_strip2d(owner, ext, rank, halo, nprocs, &h2)) {
     const long long* tile = reinterpret_cast<const long long*>(tile_scratch);
-    const long long* total = reinterpret_cast<const long long*>(
-        reinterpret_cast<char*>(tile_scratch) + ((ntiles * 8 + 255) / 256) * 256);
-    // one block per tile (a persistent grid striding over the tiles measured slower:
-    // 1.18 -> 1.56 ms at 32768^2 -- the non-empty tiles' latency chains dominate)
-    pm::k_halo2d_compact<<<(unsigned)ntiles, pm::kPartThreads, 0, (cudaStream_t)stream>>>(
-        h2, ncells, ntiles, tile, total, keys, so);
+    // warps without entries return after reading their row mask
+    const dim3 grid((unsigned)h2.nseg, (unsigned)((h2.rows + pm::kStripRows - 1) / pm::kStripRows));
+    pm::k_halo2d_compact<<<grid, pm::kPartThreads, 0, (cudaStream_t)stream>>>(
+        h2, tile, pm::strip_warp_rows(h2, tile_scratch), pm::strip_warp_pre(h2, tile_scratch),
+        keys, so);
     PM_CUDA_TRY(cudaGetLastError());
     return PM_OK;
   }

@@ -9,14 +9,18 @@
 // neighbouring GPU's `in` buffer over NVLink (peer pointers, L2-bypassing
 // loads) -- no halo buffers, no copies, no NCCL.
 //
-// Cross-GPU ordering, per neighbour (flags pushed into the reader's memory):
-//   RAW  a tile touching my rectangle's edge waits until that neighbour has
-//        finished the previous sweep (flag >= sweep); interior tiles do not;
-//   WAR  with three rotating buffers, a neighbour overwrites the buffer I
-//        read at sweep s only at its sweep s+2, so every tile just checks that
-//        neighbours finished sweep s-1 before writing (flag >= sweep - 1).
-// The last CTA of a sweep (cumulative atomic ticket) publishes "sweep done"
-// with a system-scope release store into each neighbour's flag array.
+// Cross-GPU ordering, per neighbour (flags pushed into the reader's memory; flag =
+// sweeps the writer has completed):
+//   publish  sweep s's kernel starts only after all CTAs of sweep s-1 finished
+//            (stream order), so its first CTA publishes "s sweeps done" with a
+//            system-scope release store into each neighbour's flag slot -- no
+//            per-CTA ticket atomics or fences;
+//   RAW      a tile touching my rectangle's edge waits until that neighbour
+//            has published s (finished sweep s-1); interior tiles never wait;
+//   WAR      with three rotating buffers a neighbour reads the buffer I write
+//            at sweep s during its sweep s-2.  My sweep s-1 edge tiles on that
+//            side already waited for the neighbour's flag >= s-1, i.e. for its
+//            sweep s-2 to finish, so the WAR order is implied and not checked.
 // Tiles are launched interior-first so edge tiles usually find the flag set.
 //
 // Traffic: 8 B per cell per sweep from HBM (read in, write out); vertical
@@ -95,25 +99,42 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
   const bool edge_r0 = tr == 0, edge_r1 = tr == tiles_r - 1;
   const bool edge_c0 = tc == 0, edge_c1 = tc == tiles_c - 1;
   const bool interior = !(edge_r0 || edge_r1 || edge_c0 || edge_c1);
-  if (threadIdx.x == 0) {
-    // WAR: neighbours must have finished sweep-1 before I overwrite `out`
+  const bool has_nbr = v.nbr[0] || v.nbr[1] || v.nbr[2] || v.nbr[3];
+  if (has_nbr && b == 0 && threadIdx.x == 0 && sweep > 0) {
+    // every CTA of sweep - 1 has finished: tell the neighbours
+    __threadfence_system();
     for (int d = 0; d < 4; ++d)
-      if (v.nbr[d]) wait_flag(v.my_flags + v.nbr_rank[d], sweep - 1);
-    // RAW: edge tiles read neighbour cells produced by their sweep-1
-    const bool need[4] = {edge_r0, edge_r1, edge_c0, edge_c1};
-    for (int d = 0; d < 4; ++d)
-      if (v.nbr[d] && need[d]) wait_flag(v.my_flags + v.nbr_rank[d], sweep);
+      if (v.nbr[d]) st_release_sys(v.nbr_flag_slot[d], sweep);
   }
-  __syncthreads();
+  if (!interior && has_nbr) {
+    // RAW: edge tiles read neighbour cells produced by their sweep - 1
+    if (threadIdx.x == 0) {
+      const bool need[4] = {edge_r0, edge_r1, edge_c0, edge_c1};
+      for (int d = 0; d < 4; ++d)
+        if (v.nbr[d] && need[d]) wait_flag(v.my_flags + v.nbr_rank[d], sweep);
+    }
+    __syncthreads();
+  }
 
   const int64_t r0 = (int64_t)tr * TR;
   const int64_t c = (int64_t)tc * TC + threadIdx.x * 4;
-  if (interior && (v.pitch & 3) == 0) {
-    // all neighbours local and no global boundary: rolling float4 window,
-    // 8 rows of loads in flight per thread (in/out never alias)
+  if (!(edge_r0 || edge_r1) && (v.pitch & 3) == 0 && (v.cols & 3) == 0) {
+    // rows r0-1 .. r0+TR all inside the rectangle and no Dirichlet row (only the
+    // first / last row tiles can hold one): rolling float4 window, 8 rows of loads
+    // in flight per thread (in/out never alias).  Interior tiles take every
+    // neighbour locally; in the first / last column tile the thread at the
+    // rectangle's left / right edge reads that column from the neighbour over
+    // NVLink (or keeps a Dirichlet column of the global grid).
+    if (c >= v.cols) return;
     const float* __restrict__ p = v.in + (r0 - 1) * v.pitch + c;
     float* __restrict__ po = v.out + r0 * v.pitch + c;
     const int64_t pitch = v.pitch;
+    const bool left_edge = !interior && c == 0, right_edge = !interior && c + 4 == v.cols;
+    const float* pl = left_edge && v.nbr[2]
+                          ? v.nbr[2] + r0 * v.nbr_pitch[2] + (v.nbr_cols[2] - 1) : nullptr;
+    const float* pr = right_edge && v.nbr[3] ? v.nbr[3] + r0 * v.nbr_pitch[3] : nullptr;
+    const bool g_first = left_edge && v.gcol0 == 0;
+    const bool g_last = right_edge && v.gcol0 + v.cols == v.gcols;
     float4 up = __ldg(reinterpret_cast<const float4*>(p));
     float4 mid = __ldg(reinterpret_cast<const float4*>(p + pitch));
     for (int r8 = 0; r8 < TR; r8 += 8) {
@@ -123,8 +144,10 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
       for (int u = 0; u < 8; ++u) {
         const float* row = p + (int64_t)(r8 + u + 1) * pitch;
         dn[u] = __ldg(reinterpret_cast<const float4*>(row + pitch));
-        lf[u] = __ldg(row - 1);
-        rt[u] = __ldg(row + 4);
+        lf[u] = left_edge ? (pl ? ld_peer(pl + (int64_t)(r8 + u) * v.nbr_pitch[2]) : 0.f)
+                          : __ldg(row - 1);
+        rt[u] = right_edge ? (pr ? ld_peer(pr + (int64_t)(r8 + u) * v.nbr_pitch[3]) : 0.f)
+                           : __ldg(row + 4);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -133,6 +156,8 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
         o.y = 0.25f * ((up.y + dn[u].y) + (mid.x + mid.z));
         o.z = 0.25f * ((up.z + dn[u].z) + (mid.y + mid.w));
         o.w = 0.25f * ((up.w + dn[u].w) + (mid.z + rt[u]));
+        if (g_first) o.x = mid.x;  // Dirichlet columns
+        if (g_last) o.w = mid.w;
         __stcs(reinterpret_cast<float4*>(po + (int64_t)(r8 + u) * pitch), o);
         up = mid;
         mid = dn[u];
@@ -215,19 +240,6 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
       } else {
         for (int q = 0; q < 4 && c + q < v.cols; ++q) o[q] = res[q];
       }
-    }
-  }
-  // publish "sweep done" once every CTA of this sweep has written its tile
-  if (!(v.nbr[0] || v.nbr[1] || v.nbr[2] || v.nbr[3])) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned total = gridDim.x;
-    const unsigned t = atomicAdd(v.ticket, 1u) + 1;
-    if (t == (unsigned)(sweep + 1) * total) {
-      __threadfence_system();
-      for (int d = 0; d < 4; ++d)
-        if (v.nbr[d]) st_release_sys(v.nbr_flag_slot[d], sweep + 1);
     }
   }
 }

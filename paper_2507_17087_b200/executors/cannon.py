@@ -247,4 +247,9 @@ class MappedCannon:
         return self.C[(self.step_i - 1) % 2]
 
     def close(self):
+        # captured graphs hold NCCL persistent work: release them before the
+        # communicator can be destroyed (destroy_process_group otherwise blocks)
+        if self._graphs:
+            native.require_cuda().cuda.synchronize()
+            self._graphs.clear()
         self.peers.close()

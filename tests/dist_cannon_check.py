@@ -20,6 +20,9 @@ from paper_2507_17087_b200.executors.summa import synth  # noqa: E402
 
 
 def main():
+    import faulthandler
+
+    faulthandler.dump_traceback_later(int(os.environ.get("PM_HANG_DUMP_S", "240")), exit=False)
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -35,6 +38,7 @@ def main():
                                 ("bf16", 2048, True)):
             if dtype == "fp32" and c > 1:
                 continue
+            print(f"[rank {rank}] c={c} {dtype} N={N} graph={graph}", file=sys.stderr, flush=True)
             ex = MappedCannon(N, layers=c, rank=rank, world=world, dtype=dtype, seed=21,
                               graph=graph)
             for _ in range(5):  # eager warm-up per buffer, then graph capture + replays

@@ -114,3 +114,73 @@ def test_single_call_abi_matches_compaction(cuda, ext, halo, P):
     assert torch.equal(counts, want.pair_counts)
     assert torch.equal(offsets, want.pair_offsets)
     assert torch.equal(cells[:total], want.cells) and torch.equal(dims[:total], want.dims)
+
+
+def _block_owner(rng, rows, cols, P):
+    """Random rectangular ownership: random row / column cuts, random owner per block."""
+    rc = sorted(rng.sample(range(1, rows), min(rows - 1, rng.randint(0, 3)))) if rows > 1 else []
+    cc = sorted(rng.sample(range(1, cols), min(cols - 1, rng.randint(0, 4)))) if cols > 1 else []
+    rb = [0] + rc + [rows]
+    cb = [0] + cc + [cols]
+    ids = {(a, b): rng.randrange(P) for a in range(len(rb) - 1) for b in range(len(cb) - 1)}
+    import bisect
+
+    return [[ids[(bisect.bisect_right(rb, r) - 1, bisect.bisect_right(cb, c) - 1)]
+             for c in range(cols)] for r in range(rows)]
+
+
+@pytest.mark.parametrize("rows,cols", [(37, 1028), (65, 2048), (3, 4), (1, 8), (40, 1036),
+                                       (33, 3072), (70, 516)])
+def test_strip_2d_unit_halo_matches_oracle(cuda, rows, cols):
+    """The 2-D h=(1,1) strip kernels (cols % 4 == 0): partial strips, partial row
+    blocks, single rows / columns, block and cell-level noise ownership."""
+    torch = cuda
+    rng = random.Random(rows * 7919 + cols)
+    for trial in range(2):
+        P = rng.randint(2, 8)
+        grid = _block_owner(rng, rows, cols, P)
+        if trial:  # sprinkle cell-level noise
+            for _ in range(rows * cols // 50 + 1):
+                grid[rng.randrange(rows)][rng.randrange(cols)] = rng.randrange(P)
+        flat = [v for row in grid for v in row]
+        t = torch.tensor(flat, dtype=torch.int32, device="cuda")
+        tl = halo_lists(t, (rows, cols), (1, 1), P)
+        assert _entries(tl) == O.halo_entries(lambda c: grid[c[0]][c[1]], (rows, cols), (1, 1))
+
+
+@pytest.mark.parametrize("ext,P", [((300, 4100), 7), ((129, 1024), 64), ((64, 2052), 3)])
+def test_strip_2d_out_of_range_owners_match_single_call(cuda, ext, P):
+    """Cells owned by no processor (ids < 0 or >= P) emit and receive nothing: the
+    strip kernels agree with the single-call partition of every slot."""
+    import ctypes
+
+    from paper_2507_17087_b200 import native
+
+    torch = cuda
+    g = torch.Generator(device="cuda").manual_seed(ext[1] + P)
+    n = ext[0] * ext[1]
+    owner = torch.randint(-1, P + 1, (n,), device="cuda", dtype=torch.int32, generator=g)
+    # mostly blocky: coarsen to 16x16 blocks, keep 1% noise
+    r = torch.arange(ext[0], device="cuda") // 16
+    c = torch.arange(ext[1], device="cuda") // 16
+    blk = owner.view(ext)[(r * 16).clamp(max=ext[0] - 1)][:, (c * 16).clamp(max=ext[1] - 1)]
+    noise = torch.rand(ext, device="cuda", generator=g) < 0.01
+    owner = torch.where(noise, owner.view(ext), blk).contiguous().view(-1)
+    want = halo_lists(owner, ext, (1, 1), P)
+    lib = native.lib()
+    ext_c = (ctypes.c_int64 * 2)(*ext)
+    halo_c = (ctypes.c_int32 * 2)(1, 1)
+    counts = torch.empty(P * P, dtype=torch.int64, device="cuda")
+    offsets = torch.empty(P * P, dtype=torch.int64, device="cuda")
+    nb = lib.pm_halo_scratch_bytes(ext_c, 2, P)
+    scratch = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    total = want.total
+    cells = torch.empty(max(total, 1), dtype=torch.int64, device="cuda")
+    dims = torch.empty(max(total, 1), dtype=torch.int8, device="cuda")
+    native.check(lib.pm_halo_lists(owner.data_ptr(), ext_c, 2, halo_c, P, counts.data_ptr(),
+                                   offsets.data_ptr(), cells.data_ptr(), dims.data_ptr(),
+                                   scratch.data_ptr(), nb, None), "pm_halo_lists")
+    assert total > 0
+    assert torch.equal(counts, want.pair_counts)
+    assert torch.equal(offsets, want.pair_offsets)
+    assert torch.equal(cells[:total], want.cells) and torch.equal(dims[:total], want.dims)
