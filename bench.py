@@ -478,44 +478,89 @@ def run_e2e_pipelined(args, ex):
 def run_e2e(args, ex, rank, world):
     """Same multiply through the public API with host buffers: H2D of this GPU's
     operand slices from pinned memory, the mapped multiply, D2H of its C block."""
-    import torch
-
     if world == 1:
         return run_e2e_pipelined(args, ex)
+    return run_e2e_pipelined_multi(args, ex, rank, world)
+
+
+def run_e2e_pipelined_multi(args, ex, rank, world):
+    """N > 1 end to end, pipelined like N=1 across two operand sets (two executors
+    with their own peer-shared buffers): step s loads this GPU's A / B slices into
+    set s % 2 from pinned memory (H2D stream), a stream-ordered 4-byte NCCL
+    all-reduce on a comm stream says "every GPU's slices landed" before any pull
+    of step s, the mapped multiply runs, a second all-reduce says "every GPU is
+    done pulling from set s % 2" before step s + 2 overwrites it, and C goes out
+    on the D2H stream.  No host synchronisation inside the window; CUDA events
+    from the first H2D to the last D2H, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_17087_b200.executors.summa import MappedGemm
 
     lay = ex.layout
     ka, kb = lay.a_slice[rank], lay.b_slice[rank]
+    ex2 = MappedGemm(ex.M, ex.N, ex.K, mapping=ex.mapping, rank=rank, world=world,
+                     a_chunks=args.chunks)
+    sets = [ex, ex2]
     hA = ex.A[:, ka[0]:ka[1]].contiguous().cpu().pin_memory()
     hB = ex.Bt[:, kb[0]:kb[1]].contiguous().cpu().pin_memory()
-    hC = torch.empty(ex.C.shape, dtype=ex.C.dtype).pin_memory()
+    hC = [torch.empty(ex.C.shape, dtype=ex.C.dtype).pin_memory() for _ in range(2)]
     cs = torch.cuda.current_stream()
+    h2d, d2h, comm = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    flag = torch.zeros(2, dtype=torch.int32, device=cs.device)
+    ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "ready", "comp", "free", "out")}
+    for b in range(2):
+        for k in ("comp", "free", "out"):
+            ev[k][b].record(cs)
 
-    def step():
-        ex.A[:, ka[0]:ka[1]].copy_(hA, non_blocking=True)
-        ex.Bt[:, kb[0]:kb[1]].copy_(hB, non_blocking=True)
-        if world > 1:  # peers may pull these slices only once they have landed
-            torch.cuda.synchronize()
-            barrier(world)
-        ex.step()
-        hC.copy_(ex.C, non_blocking=True)
+    def run(n, t0=None, t1=None):
+        if t0 is not None:
+            t0.record(h2d)
+        for s in range(n):
+            b = s % 2
+            E = sets[b]
+            h2d.wait_event(ev["free"][b])      # every GPU done pulling from set b
+            with torch.cuda.stream(h2d):
+                E.A[:, ka[0]:ka[1]].copy_(hA, non_blocking=True)
+                E.Bt[:, kb[0]:kb[1]].copy_(hB, non_blocking=True)
+            ev["in"][b].record(h2d)
+            comm.wait_event(ev["in"][b])
+            with torch.cuda.stream(comm):     # every GPU's slices of set b landed
+                dist.all_reduce(flag[0:1])
+            ev["ready"][b].record(comm)
+            cs.wait_event(ev["out"][b])        # C of two steps ago has been read out
+            E.step(stream=cs, ready=ev["ready"][b])
+            ev["comp"][b].record(cs)
+            comm.wait_event(ev["comp"][b])
+            with torch.cuda.stream(comm):
+                dist.all_reduce(flag[1:2])
+            ev["free"][b].record(comm)
+            d2h.wait_event(ev["comp"][b])
+            with torch.cuda.stream(d2h):
+                hC[b].copy_(E.C, non_blocking=True)
+            ev["out"][b].record(d2h)
+        if t1 is not None:
+            t1.record(d2h)
 
-    for _ in range(1):
-        step()
+    run(2)
     torch.cuda.synchronize()
     barrier(world)
-    n = max(1, min(args.steps, 3))
+    n = min(max(8, args.steps), 32)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record(cs)
-    for _ in range(n):
-        step()
-    t1.record(cs)
+    run(n, t0, t1)
     torch.cuda.synchronize()
     ms = max_over_ranks(t0.elapsed_time(t1) / n, world)
-    h2d = sum_over_ranks(hA.numel() * 2 + hB.numel() * 2, world)
-    d2h = sum_over_ranks(hC.numel() * hC.element_size(), world)
+    barrier(world)
+    ex2.close()
+    del ex2
+    torch.cuda.empty_cache()
+    h2d_b = sum_over_ranks(hA.numel() * 2 + hB.numel() * 2, world)
+    d2h_b = sum_over_ranks(hC[0].numel() * hC[0].element_size(), world)
     S = args.size
     return {"value": 2 * S ** 3 / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+            "steps": n, "h2d_bytes_per_step": int(h2d_b), "d2h_bytes_per_step": int(d2h_b),
+            "pipelined": "two operand sets: H2D(s+1) / mapped multiply(s) / D2H(s-1) on "
+                         "separate streams, stream-ordered NCCL flags between GPUs"}
 
 
 def cpu_sample(args, threads=None):

@@ -298,14 +298,19 @@ class MappedGemm:
         dst = self.peers.ptrs[name][self.rank] + (row0 * self.K + k0) * esz
         copy2d(dst, pitch, src, pitch, (k1 - k0) * esz, nrows, stream)
 
-    def step(self, stream=None):
-        """One full multiply, stream-ordered (no host synchronisation)."""
+    def step(self, stream=None, ready=None):
+        """One full multiply, stream-ordered (no host synchronisation).  `ready`: an
+        optional event the pulls also wait for (e.g. every GPU's operands landed)."""
         torch = native.require_cuda()
         from ..gemm import tile_gemm
 
         cs = stream or torch.cuda.current_stream()
         for s in self.copy_streams:
             s.wait_event(self.done)  # the previous multiply no longer reads A / Bt
+            if ready is not None:
+                s.wait_event(ready)
+        if ready is not None:
+            cs.wait_event(ready)
         for name, q, row0, rows, k0, k1, si, ev in self.pulls:
             s = self.copy_streams[si]
             self._copy(name, q, row0, rows, k0, k1, s)
