@@ -77,7 +77,11 @@ int pm_map_hist(pm_plan* plan, const int32_t* points, int64_t n, int64_t first, 
   int nb = nbins;
   void* args[] = {(void*)&pts, (void*)&nn, (void*)&ff, (void*)&nb, (void*)&ntiles,
                   (void*)&hist, (void*)&status};
-  PM_CU_TRY(d->launchKernel(plan->fn_hist, (unsigned)ntiles, 1, 1, pm::kPartThreads, 1, 1,
+  // grid-stride over groups of 256 tiles (tiles proven uniform cost one thread each)
+  long long groups = (ntiles + pm::kPartThreads - 1) / pm::kPartThreads;
+  const long long cap = (long long)pm::num_sms() * 8;
+  if (groups > cap) groups = cap;
+  PM_CU_TRY(d->launchKernel(plan->fn_hist, (unsigned)groups, 1, 1, pm::kPartThreads, 1, 1,
                             (unsigned)smem, (CUstream)s, args, nullptr));
   if ((rc = pm::exclusive_scan_i64(hist, len, scan_tmp, s))) return rc;
   pm::k_part_bin_totals<<<(nbins + 255) / 256, 256, 0, s>>>(

@@ -44,6 +44,8 @@ template <typename T> __device__ __forceinline__ T pm_fmod(T a, T b) {
   return (r != 0 && ((r < 0) != (b < 0))) ? r + b : r;
 }
 #define PM_FAIL(s) do { *site_out = (s); return -1; } while (0)
+template <typename T> __device__ __forceinline__ T pm_min2(T a, T b) { return a < b ? a : b; }
+template <typename T> __device__ __forceinline__ T pm_max2(T a, T b) { return a > b ? a : b; }
 )CUDA";
 
 struct Gen {
@@ -181,6 +183,127 @@ struct Gen {
     }
   }
 
+  // Interval version of the point program over a box of coordinates [bl_i, bh_i]
+  // (registers l<r> / h<r>): returns the bin if every point of the box provably
+  // maps to it without failure, else -1 ("not proven").  Each register's tile
+  // interval lies inside the host's static interval for it, so the endpoint
+  // arithmetic never leaves the register widths the host chose.  Floor division
+  // is monotone in each argument while the divisor keeps its sign, so its
+  // extremes sit at the corners; a condition that is not decided over the box,
+  // a check that may fail, a reachable failure or a possibly-zero divisor gives
+  // up.
+  void ibody() {
+    for (int i = 0; i < p->n_insns; ++i) {
+      const pm_insn& in = p->insns[i];
+      const int d = in.dst;
+      const char* T = kSigned[in.op == PM_OP_CHECK || in.op == PM_OP_IF || in.op == PM_OP_RET ||
+                                      in.op == PM_OP_FAIL || in.op == PM_OP_ELSE ||
+                                      in.op == PM_OP_ENDIF ? 0 : w(d)];
+      const char* U = kUnsigned[in.op == PM_OP_CHECK || in.op == PM_OP_IF || in.op == PM_OP_RET ||
+                                        in.op == PM_OP_FAIL || in.op == PM_OP_ELSE ||
+                                        in.op == PM_OP_ENDIF ? 0 : w(d)];
+      auto L = [&](int r) { return "l" + std::to_string(r); };
+      auto H = [&](int r) { return "h" + std::to_string(r); };
+      auto cast = [&](const std::string& x) { return std::string("(") + T + ")(" + x + ")"; };
+      auto ucast = [&](const std::string& x) { return std::string("(") + U + ")(" + x + ")"; };
+      switch (in.op) {
+        case PM_OP_CONST: {
+          const std::string c = cst(w(d), in.lo, in.hi);
+          o << "  " << L(d) << " = " << c << "; " << H(d) << " = " << c << ";\n";
+          break;
+        }
+        case PM_OP_COORD:
+          o << "  " << L(d) << " = (" << T << ")bl" << in.lo << "; " << H(d) << " = (" << T
+            << ")bh" << in.lo << ";\n";
+          break;
+        case PM_OP_ADD:
+          o << "  " << L(d) << " = " << cast(ucast(L(in.a)) + " + " + ucast(L(in.b))) << "; "
+            << H(d) << " = " << cast(ucast(H(in.a)) + " + " + ucast(H(in.b))) << ";\n";
+          break;
+        case PM_OP_SUB:
+          o << "  " << L(d) << " = " << cast(ucast(L(in.a)) + " - " + ucast(H(in.b))) << "; "
+            << H(d) << " = " << cast(ucast(H(in.a)) + " - " + ucast(L(in.b))) << ";\n";
+          break;
+        case PM_OP_MUL: {
+          o << "  { const " << T << " p0 = " << cast(ucast(L(in.a)) + " * " + ucast(L(in.b)))
+            << ", p1 = " << cast(ucast(L(in.a)) + " * " + ucast(H(in.b)))
+            << ", p2 = " << cast(ucast(H(in.a)) + " * " + ucast(L(in.b)))
+            << ", p3 = " << cast(ucast(H(in.a)) + " * " + ucast(H(in.b))) << "; "
+            << L(d) << " = pm_min2(pm_min2(p0, p1), pm_min2(p2, p3)); " << H(d)
+            << " = pm_max2(pm_max2(p0, p1), pm_max2(p2, p3)); }\n";
+          break;
+        }
+        case PM_OP_DIV: case PM_OP_MOD: {
+          const int cw = std::max(w(d), std::max(w(in.a), w(in.b)));
+          const char* ct = kSigned[cw];
+          o << "  { const " << ct << " xa = (" << ct << ")" << L(in.a) << ", xb = (" << ct << ")"
+            << H(in.a) << ", ya = (" << ct << ")" << L(in.b) << ", yb = (" << ct << ")"
+            << H(in.b) << "; if (ya <= 0 && yb >= 0) return -1; ";
+          if (in.op == PM_OP_DIV) {
+            o << "const " << ct << " q0 = pm_fdiv(xa, ya), q1 = pm_fdiv(xa, yb), q2 = "
+              << "pm_fdiv(xb, ya), q3 = pm_fdiv(xb, yb); " << L(d) << " = (" << T
+              << ")pm_min2(pm_min2(q0, q1), pm_min2(q2, q3)); " << H(d) << " = (" << T
+              << ")pm_max2(pm_max2(q0, q1), pm_max2(q2, q3)); }\n";
+          } else {
+            o << "if (ya == yb && pm_fdiv(xa, ya) == pm_fdiv(xb, ya)) { " << L(d) << " = (" << T
+              << ")pm_fmod(xa, ya); " << H(d) << " = (" << T << ")pm_fmod(xb, ya); } "
+              << "else if (ya > 0) { " << L(d) << " = 0; " << H(d) << " = (" << T
+              << ")(yb - 1); } else { " << L(d) << " = (" << T << ")(ya + 1); " << H(d)
+              << " = 0; } }\n";
+          }
+          break;
+        }
+        case PM_OP_GT: case PM_OP_LT: case PM_OP_EQ: {
+          const int cw = std::max(w(in.a), w(in.b));
+          const char* ct = kSigned[cw];
+          const std::string la = std::string("(") + ct + ")" + L(in.a), ha = std::string("(") + ct + ")" + H(in.a);
+          const std::string lb = std::string("(") + ct + ")" + L(in.b), hb = std::string("(") + ct + ")" + H(in.b);
+          std::string yes, no;
+          if (in.op == PM_OP_GT) { yes = la + " > " + hb; no = ha + " <= " + lb; }
+          else if (in.op == PM_OP_LT) { yes = ha + " < " + lb; no = la + " >= " + hb; }
+          else { yes = "(" + la + " == " + ha + " && " + lb + " == " + hb + " && " + la + " == " + lb + ")";
+                 no = "(" + ha + " < " + lb + " || " + hb + " < " + la + ")"; }
+          o << "  if (" << yes << ") { " << L(d) << " = 1; " << H(d) << " = 1; } else if (" << no
+            << ") { " << L(d) << " = 0; " << H(d) << " = 0; } else { " << L(d) << " = 0; "
+            << H(d) << " = 1; }\n";
+          break;
+        }
+        case PM_OP_SELECT:
+          o << "  if (" << L(in.a) << " > 0 || " << H(in.a) << " < 0) { " << L(d) << " = (" << T
+            << ")" << L(in.b) << "; " << H(d) << " = (" << T << ")" << H(in.b) << "; } else if ("
+            << L(in.a) << " == 0 && " << H(in.a) << " == 0) { " << L(d) << " = (" << T << ")"
+            << L(in.c) << "; " << H(d) << " = (" << T << ")" << H(in.c) << "; } else { " << L(d)
+            << " = pm_min2((" << T << ")" << L(in.b) << ", (" << T << ")" << L(in.c) << "); "
+            << H(d) << " = pm_max2((" << T << ")" << H(in.b) << ", (" << T << ")" << H(in.c)
+            << "); }\n";
+          break;
+        case PM_OP_MOV:
+          o << "  " << L(d) << " = (" << T << ")" << L(in.a) << "; " << H(d) << " = (" << T
+            << ")" << H(in.a) << ";\n";
+          break;
+        case PM_OP_CHECK: {
+          const int cw = std::max(w(in.a), (in.lo < INT_MIN || in.hi > INT_MAX) ? 1 : 0);
+          const char* ct = kSigned[cw];
+          o << "  if ((" << ct << ")" << L(in.a) << " < (" << ct << ")" << in.lo << "LL || ("
+            << ct << ")" << H(in.a) << " >= (" << ct << ")" << in.hi << "LL) return -1;\n";
+          break;
+        }
+        case PM_OP_FAIL: o << "  return -1;\n"; break;
+        case PM_OP_IF:
+          o << "  { const int t_ = (" << L(in.a) << " > 0 || " << H(in.a) << " < 0) ? 1 : ("
+            << L(in.a) << " == 0 && " << H(in.a) << " == 0) ? 0 : -1; if (t_ < 0) return -1; "
+            << "if (t_) {\n";
+          break;
+        case PM_OP_ELSE: o << "  } else {\n"; break;
+        case PM_OP_ENDIF: o << "  } }\n"; break;
+        case PM_OP_RET:
+          o << "  return (" << L(in.a) << " == " << H(in.a) << " && " << L(in.a) << " >= 0 && "
+            << L(in.a) << " <= 0x7FFFFFFF) ? (int)" << L(in.a) << " : -1;\n";
+          break;
+      }
+    }
+  }
+
   // Width (0/1) of the implicit row-major index and coordinate types.
   bool implicit_wide() const {
     unsigned long long total = 1;
@@ -228,6 +351,45 @@ struct Gen {
     o << "  return pm_point(";
     for (int i = 0; i < k; ++i) o << "c" << i << ", ";
     o << "site);\n}\n\n";
+
+    // pm_tile_bin(lin0, cnt): the bin shared by every point of [lin0, lin0 + cnt),
+    // proven over the row-major coordinate box of that range, or -1
+    o << "__device__ __noinline__ int pm_tile_box(";
+    for (int i = 0; i < k; ++i) o << "long long bl" << i << ", long long bh" << i << ", ";
+    o << "int unused_) {\n";
+    for (int r = 0; r < p->n_regs; ++r)
+      o << "  " << kSigned[w(r)] << " l" << r << " = 0, h" << r << " = 0;\n";
+    ibody();
+    o << "  return -1;\n}\n\n";
+    o << "__device__ __forceinline__ int pm_tile_bin(long long lin0, long long cnt) {\n";
+    if (!impl) {
+      o << "  (void)lin0; (void)cnt; return -1;\n}\n\n";
+    } else {
+      for (int i = 0; i < k; ++i) o << "  long long cf" << i << ", cl" << i << ";\n";
+      for (int e = 0; e < 2 && k > 0; ++e) {
+        const char* nm = e ? "cl" : "cf";
+        o << "  { " << it << " t = (" << it << ")(lin0" << (e ? " + cnt - 1" : "") << ");\n";
+        for (int i = k - 1; i >= 0; --i) {
+          if (i == 0) {
+            o << "    " << nm << "0 = (long long)t;\n";
+          } else {
+            o << "    " << nm << i << " = (long long)(t % (" << it << ")" << p->extents[i]
+              << "ULL); t /= (" << it << ")" << p->extents[i] << "ULL;\n";
+          }
+        }
+        o << "  }\n";
+      }
+      o << "  int diff_ = 0;\n";
+      for (int i = 0; i < k; ++i) {
+        o << "  long long bl" << i << ", bh" << i << ";\n";
+        o << "  if (diff_) { bl" << i << " = 0; bh" << i << " = " << (p->extents[i] - 1)
+          << "LL; } else { bl" << i << " = cf" << i << "; bh" << i << " = cl" << i
+          << "; diff_ = cf" << i << " != cl" << i << "; }\n";
+      }
+      o << "  return pm_tile_box(";
+      for (int i = 0; i < k; ++i) o << "bl" << i << ", bh" << i << ", ";
+      o << "0);\n}\n\n";
+    }
 
     const int K = impl ? 0 : k;
     o << "#define PM_K " << K << "\n";
@@ -300,6 +462,9 @@ struct PmMapKey {
   int nbins;
   static constexpr bool kVec4 = false;
   static constexpr bool kPeek = true;
+  __device__ __forceinline__ int tile_bin(long long base, long long count) const {
+    return pm_tile_bin(first + base, count);
+  }
   __device__ __forceinline__ int peek(long long i) const {
     int site = 0;
     return pm_eval(first + i, pts + i * PM_K, &site);
@@ -349,7 +514,7 @@ pm_map_hist(const int* pts, long long n, long long first, int nbins, long long n
             long long* __restrict__ hist, unsigned long long* status) {
   extern __shared__ __align__(16) int smem_words[];
   const PmMapKey key{pts, first, status, nullptr, nbins};
-  pmdev::small_hist_body(key, n, nbins, ntiles, hist, smem_words);
+  pmdev::small_hist_proof(key, n, nbins, ntiles, hist, smem_words);
 }
 
 extern "C" __global__ void __launch_bounds__(256, 6)
@@ -358,7 +523,8 @@ pm_map_scatter(const int* pts, long long n, long long first, int nbins, long lon
                int* perm, long long base) {
   extern __shared__ __align__(16) int smem_words[];
   const PmMapKey key{pts, first, status, out, nbins};
-  pmdev::small_scatter_body(key, PmPermSink{perm, base}, n, nbins, ntiles, pos0, smem_words);
+  pmdev::small_scatter_body(key, PmPermSink{perm, base}, n, nbins, ntiles, pos0, smem_words,
+                            (long long)blockIdx.x);
 }
 
 extern "C" __global__ void __launch_bounds__(256, 6)
@@ -367,7 +533,8 @@ pm_map_scatter_peer(const int* pts, long long n, long long first, int nbins, lon
                     const long long* tab, long long base) {
   extern __shared__ __align__(16) int smem_words[];
   const PmMapKey key{pts, first, status, out, nbins};
-  pmdev::small_scatter_body(key, PmPeerSink{tab, base}, n, nbins, ntiles, pos0, smem_words);
+  pmdev::small_scatter_body(key, PmPeerSink{tab, base}, n, nbins, ntiles, pos0, smem_words,
+                            (long long)blockIdx.x);
 }
 )CUDA";
 

@@ -97,13 +97,13 @@ __device__ __forceinline__ const int* tile_info_of(const long long* hist, int nb
 template <class Key>
 __device__ __forceinline__ void small_hist_body(const Key& key, long long n, int nbins,
                                                 long long ntiles, long long* __restrict__ hist,
-                                                int* smem_words) {
+                                                int* smem_words, long long tile) {
   int* h = smem_words;
   __shared__ int s_only, s_any;
   if (threadIdx.x == 0) s_only = kTileMixed, s_any = 0;
   for (int b = threadIdx.x; b < kPartWarps * nbins; b += kPartThreads) h[b] = 0;
   __syncthreads();
-  const long long base = (long long)blockIdx.x * kSmallTile;
+  const long long base = tile * kSmallTile;
   int* hw = h + (threadIdx.x >> 5) * nbins;
   int run_bin = -1, run = 0;
   auto add = [&](int b) {
@@ -158,18 +158,50 @@ __device__ __forceinline__ void small_hist_body(const Key& key, long long n, int
     int sum = 0;
 #pragma unroll
     for (int w = 0; w < kPartWarps; ++w) sum += h[w * nbins + b];
-    hist[(long long)b * ntiles + blockIdx.x] = sum;
+    hist[(long long)b * ntiles + tile] = sum;
     if (sum) s_any = 1;
     if (sum == kSmallTile) s_only = b;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     // the last (possibly partial) tile always takes the general path
-    const int info = blockIdx.x + 1 == ntiles ? kTileMixed
-                     : s_only >= 0            ? s_only
-                     : s_any                  ? kTileMixed
-                                              : kTileEmpty;
-    const_cast<int*>(tile_info_of(hist, nbins, ntiles))[blockIdx.x] = info;
+    const int info = tile + 1 == ntiles ? kTileMixed
+                     : s_only >= 0       ? s_only
+                     : s_any             ? kTileMixed
+                                         : kTileEmpty;
+    const_cast<int*>(tile_info_of(hist, nbins, ntiles))[tile] = info;
+  }
+}
+
+// Histogram pass for keys that can prove a whole tile's bin without evaluating
+// its points (Key::tile_bin(base, count) -> the bin, or -1 if not proven; the
+// generated mapping programs do it by interval arithmetic over the tile's
+// coordinate box).  Grid-stride over groups of 256 tiles: every thread tries
+// to prove one tile and, on success, writes its histogram column and tile_info
+// (a uniform tile: pass 2 writes its indices without evaluating anything);
+// the CTA then histograms the unproven tiles of the group point by point.
+// The last (possibly partial) tile always takes the general path.
+template <class Key>
+__device__ __forceinline__ void small_hist_proof(const Key& key, long long n, int nbins,
+                                                 long long ntiles, long long* __restrict__ hist,
+                                                 int* smem_words) {
+  __shared__ int s_todo[kPartThreads];
+  int* info = const_cast<int*>(tile_info_of(hist, nbins, ntiles));
+  const long long ngroups = (ntiles + kPartThreads - 1) / kPartThreads;
+  for (long long g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const long long t = g * kPartThreads + threadIdx.x;
+    int b = -1;
+    if (t + 1 < ntiles) b = key.tile_bin(t * kSmallTile, kSmallTile);
+    if (b >= nbins) b = -1;
+    if (b >= 0) {
+      for (int q = 0; q < nbins; ++q) hist[(long long)q * ntiles + t] = q == b ? kSmallTile : 0;
+      info[t] = b;
+    }
+    s_todo[threadIdx.x] = t < ntiles && b < 0;
+    __syncthreads();
+    for (int j = 0; j < kPartThreads; ++j)
+      if (s_todo[j]) small_hist_body(key, n, nbins, ntiles, hist, smem_words, g * kPartThreads + j);
+    __syncthreads();
   }
 }
 
@@ -179,22 +211,22 @@ template <class Key, class Sink>
 __device__ __forceinline__ void small_scatter_body(const Key& key, const Sink& sink, long long n,
                                                    int nbins, long long ntiles,
                                                    const long long* __restrict__ pos0,
-                                                   int* smem_words) {
+                                                   int* smem_words, long long tile) {
   signed char* sbin = reinterpret_cast<signed char*>(smem_words);
   short* stage = reinterpret_cast<short*>(sbin + kSmallTile);
   int* cnt = reinterpret_cast<int*>(stage + kSmallTile);
   int* start = cnt + nbins * kPartThreads;
-  const long long base = (long long)blockIdx.x * kSmallTile;
+  const long long base = tile * kSmallTile;
   // The histogram pass left a summary of every tile (tile_info): a tile with no
   // output at all (every key -1: e.g. interior cells of a halo launch) is
   // skipped; a full tile whose 4096 items all share one bin (block mappings,
   // the common case) is a straight copy of consecutive indices -- in neither
   // case is a key evaluated or read.
-  const int info = __ldg(tile_info_of(pos0, nbins, ntiles) + blockIdx.x);
+  const int info = __ldg(tile_info_of(pos0, nbins, ntiles) + tile);
   if (info == kTileEmpty) return;
   if (info >= 0) {
     const int only = info;
-    const long long p0 = pos0[(long long)only * ntiles + blockIdx.x];
+    const long long p0 = pos0[(long long)only * ntiles + tile];
     key.uniform(base, kSmallTile, only);
     sink.put_run(only, p0, base, kSmallTile);
     return;
@@ -267,7 +299,7 @@ __device__ __forceinline__ void small_scatter_body(const Key& key, const Sink& s
   for (int b = 0; b < nbins; ++b)
     if (start[b + 1] - start[b] == kSmallTile) only = b;
   if (only >= 0) {
-    const long long p0 = pos0[(long long)only * ntiles + blockIdx.x];
+    const long long p0 = pos0[(long long)only * ntiles + tile];
 #pragma unroll 4
     for (int k = threadIdx.x; k < kSmallTile; k += kPartThreads) sink.put(only, p0 + k, base + k);
     return;
@@ -287,7 +319,7 @@ __device__ __forceinline__ void small_scatter_body(const Key& key, const Sink& s
   for (int b = warp; b < nbins; b += kPartWarps) {
     const int lo = start[b], hi = start[b + 1];
     if (lo == hi) continue;
-    const long long p0 = pos0[(long long)b * ntiles + blockIdx.x] - lo;
+    const long long p0 = pos0[(long long)b * ntiles + tile] - lo;
     for (int k = lo + lane; k < hi; k += 32) sink.put(b, p0 + k, base + stage[k]);
   }
 }

@@ -140,7 +140,7 @@ template <class Key>
 __global__ void __launch_bounds__(kPartThreads)
 k_small_hist(Key key, long long n, int nbins, long long ntiles, long long* __restrict__ hist) {
   extern __shared__ __align__(16) int smem_words[];
-  pmdev::small_hist_body(key, n, nbins, ntiles, hist, smem_words);
+  pmdev::small_hist_body(key, n, nbins, ntiles, hist, smem_words, (long long)blockIdx.x);
 }
 
 // (min 6 CTAs / SM: the uniform-tile copy is a pure store stream, occupancy-bound)
@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(kPartThreads, 6)
 k_small_scatter(Key key, Sink sink, long long n, int nbins, long long ntiles,
                 const long long* __restrict__ pos0) {
   extern __shared__ __align__(16) int smem_words[];
-  pmdev::small_scatter_body(key, sink, n, nbins, ntiles, pos0, smem_words);
+  pmdev::small_scatter_body(key, sink, n, nbins, ntiles, pos0, smem_words,
+                            (long long)blockIdx.x);
 }
 
 inline size_t small_hist_smem(int nbins) {
@@ -179,7 +180,8 @@ int stable_partition_small(Key key, Sink sink, bool scatter, long long n, int nb
   if (smem_s > 48 * 1024)
     PM_CUDA_TRY(cudaFuncSetAttribute(k_small_scatter<Key, Sink>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
-  k_small_hist<Key><<<(unsigned)ntiles, kPartThreads, smem_h, s>>>(key, n, nbins, ntiles, hist);
+  k_small_hist<Key><<<(unsigned)ntiles, kPartThreads, smem_h, s>>>(key, n, nbins, ntiles,
+                                                                       hist);
   PM_CUDA_TRY(cudaGetLastError());
   int rc = exclusive_scan_i64(hist, len, scan_tmp, s);
   if (rc) return rc;
@@ -187,8 +189,8 @@ int stable_partition_small(Key key, Sink sink, bool scatter, long long n, int nb
       hist, ntiles, nbins, reinterpret_cast<const long long*>(scan_tmp), counts, offsets);
   PM_CUDA_TRY(cudaGetLastError());
   if (scatter) {
-    k_small_scatter<Key, Sink><<<(unsigned)ntiles, kPartThreads, smem_s, s>>>(key, sink, n,
-                                                                             nbins, ntiles, hist);
+    k_small_scatter<Key, Sink><<<(unsigned)ntiles, kPartThreads, smem_s, s>>>(
+        key, sink, n, nbins, ntiles, hist);
     PM_CUDA_TRY(cudaGetLastError());
   }
   return PM_OK;

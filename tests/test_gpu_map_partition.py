@@ -103,3 +103,88 @@ def test_fused_full_stencil_launch(cuda):
     own = fn.map_partition((L, L))
     assert torch.equal(own.counts, ref.counts)
     assert torch.equal(own.perm, ref.perm)
+
+
+def _scaled(ispace, min_points=3 * 4096 + 123):
+    """The golden launch shape stretched to several 4096-point tiles."""
+    n = 1
+    for e in ispace:
+        n *= e
+    f = 1
+    while n * f ** len(ispace) < min_points:
+        f += 1
+    return tuple(e * f + (i % 2) for i, e in enumerate(ispace))
+
+
+def test_tile_proofs_on_multi_tile_launches(cuda):
+    """Pass 1 proves whole tiles uniform by interval arithmetic over each tile's
+    coordinate box (mapping.cpp pm_tile_bin); only tiles before the last are
+    eligible, so the golden launches (one tile) never exercise it.  Stretch the
+    golden programs -- corpus mappers and the seeded random programs with
+    ternaries, negative operands, division / modulo by zero, helper calls -- to
+    multi-tile launches and hold the fused partition to K1 then K2, errors
+    included."""
+    torch = cuda
+    done = 0
+    for c in CASES[1::13]:
+        machine = MachineShape("GPU", *c["machine"])
+        fn = compile_mapper(parse(c["source"]), c["task"], machine)
+        ispace = _scaled(tuple(c["ispace"]))
+        P = machine.nodes * machine.procs_per_node
+        try:
+            ids = fn.map_ispace(ispace)
+        except Exception as e1:  # noqa: BLE001
+            with pytest.raises(Exception) as e2:
+                fn.map_partition(ispace)
+            assert type(e1) is type(e2.value) and str(e1) == str(e2.value), c["name"]
+            continue
+        own = fn.map_partition(ispace)
+        assert _same(own, partition(ids, P)), (c["name"], ispace)
+        done += 1
+    assert done > 20
+
+
+PROOF_EDGES = """
+m = Machine(GPU)
+def blk(Tuple p, Tuple s):
+    q = m.merge(0, 1).decompose(0, s)
+    return q[*(p * q.size / s)]
+def tern(Tuple p, Tuple s):
+    q = m.merge(0, 1)
+    return q[(p[0] > 50 ? 1 : (p[1] < 4000 ? 0 : 2))]
+def divp(Tuple p, Tuple s):
+    q = m.merge(0, 1)
+    return q[(1000 / (p[0] - 97)) % q.size[0]]
+def neg(Tuple p, Tuple s):
+    q = m.merge(0, 1)
+    return q[((p[1] - 5000) / 777) % q.size[0]]
+def rowmod(Tuple p, Tuple s):
+    q = m.merge(0, 1)
+    return q[(p[0] / 3 + p[1] / 4096) % q.size[0]]
+IndexTaskMap blk blk
+IndexTaskMap tern tern
+IndexTaskMap divp divp
+IndexTaskMap neg neg
+IndexTaskMap rowmod rowmod
+"""
+
+
+@pytest.mark.parametrize("task", ["blk", "tern", "divp", "neg", "rowmod"])
+@pytest.mark.parametrize("ispace", [(200, 8192), (150, 10007), (3, 4096 * 5 + 1)])
+def test_tile_proof_edges(cuda, task, ispace):
+    """Tiles straddling block edges, decided / undecided ternaries, a divisor
+    that is zero on one row (an error at the lowest failing point, as K1),
+    floor division of negative values, and row-periodic modulo."""
+    machine = MachineShape("GPU", 2, 3)
+    fn = compile_mapper(parse(PROOF_EDGES), task, machine)
+    try:
+        ids = fn.map_ispace(ispace)
+    except Exception as e1:  # noqa: BLE001
+        with pytest.raises(Exception) as e2:
+            fn.map_partition(ispace)
+        assert type(e1) is type(e2.value) and str(e1) == str(e2.value)
+        return
+    assert _same(fn.map_partition(ispace), partition(ids, 6))
+    f0, cnt = 4096 * 3 + 5, 4096 * 7 + 9  # a sub-range: tiles start off the launch's grid
+    assert _same(fn.map_partition(ispace, first=f0, count=cnt),
+                 partition(ids[f0:f0 + cnt].contiguous(), 6))
