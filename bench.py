@@ -161,13 +161,14 @@ def sum_over_ranks(x: float, world: int) -> float:
 # -- our implementation -----------------------------------------------------------------
 
 
-def run_mapping(args, rank, world, local, mapping, timed=True):
+def run_mapping(args, rank, world, local, mapping, mnk=None):
     import torch
 
     from paper_2507_17087_b200.executors.summa import MappedGemm
 
     S = args.size
-    ex = MappedGemm(S, S, S, mapping=mapping, rank=rank, world=world, a_chunks=args.chunks,
+    M, N, K = mnk or (S, S, S)
+    ex = MappedGemm(M, N, K, mapping=mapping, rank=rank, world=world, a_chunks=args.chunks,
                     seed=1234)
     cs = torch.cuda.current_stream()
     sampler = ClockSampler(local).start()
@@ -219,7 +220,7 @@ def run_mapping(args, rank, world, local, mapping, timed=True):
     res = {
         "grid": list(ex.layout.grid),
         "ms_per_step": ms_max,
-        "tflops": 2 * S ** 3 / (ms_max * 1e-3) / 1e12,
+        "tflops": 2 * M * N * K / (ms_max * 1e-3) / 1e12,
         "comm_bytes_per_gpu_max": int(max_over_ranks(ex.recv_bytes, world)),
         "comm_bytes_total": int(sum_over_ranks(ex.recv_bytes, world)),
         "gemm_launch_ms_avg": statistics.mean(launch_ms),
@@ -263,20 +264,19 @@ def run_3d(args, rank, world, local, M, N, K, mapping):
     return res
 
 
-def run_cannon(args, rank, world, N, layers, dtype):
+def run_cannon(args, rank, world, N, layers, dtype, graph=False):
     """BASELINE configs[0] (Cannon fp32 N=1024 on 2x2) and the Cannon / 2.5D
     bf16 variants: Cannon skew + shifts as NVLink pulls, 2.5D layer reduction
-    fused into the GEMM epilogue."""
+    fused into the GEMM epilogue.  graph=True replays the whole multiply (pulls,
+    peer-memory barriers, GEMMs) as one CUDA graph per C buffer."""
     import torch
 
     from paper_2507_17087_b200.executors.cannon import MappedCannon, cannon_moves
 
-    # (CUDA-graph replay of the whole multiply is supported -- MappedCannon(graph=True) --
-    # but measured slower at configs[0] on 4 GPUs: 0.35 vs 0.14 ms, the captured NCCL
-    # barriers dominate; the eager path is timed)
-    ex = MappedCannon(N, layers=layers, rank=rank, world=world, dtype=dtype, seed=31)
+    ex = MappedCannon(N, layers=layers, rank=rank, world=world, dtype=dtype, seed=31,
+                      graph=graph)
     cs = torch.cuda.current_stream()
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 4 if graph else 0)):  # graphs are captured in warm-up
         ex.step()
     ex.result()
     torch.cuda.synchronize()
@@ -291,7 +291,8 @@ def run_cannon(args, rank, world, N, layers, dtype):
     torch.cuda.synchronize()
     ms = max_over_ranks(t0.elapsed_time(t1) / steps, world)
     moves = int(sum_over_ranks(ex.moved_blocks, world))
-    res = {"N": N, "dtype": dtype, "grid": [ex.q, ex.q, ex.c], "machine": list(ex.machine),
+    res = {"N": N, "dtype": dtype, "graph": graph, "grid": [ex.q, ex.q, ex.c],
+           "machine": list(ex.machine),
            "ms_per_multiply": ms, "tflops": 2.0 * N ** 3 / (ms * 1e-3) / 1e12,
            "block_moves": moves, "block_moves_schedule": cannon_moves(ex.q, ex.c),
            "bytes_moved": moves * ex.block_bytes}
@@ -467,9 +468,24 @@ def run_e2e_pipelined(args, ex):
     e1.record(d2h)
     torch.cuda.synchronize()
     d2h_ms = e0.elapsed_time(e1)
+    # both directions at once, no GEMM: the PCIe / host-memory floor of a pipelined step
+    e2 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(h2d)
+    d2h.wait_event(e0)
+    with torch.cuda.stream(h2d):
+        bufs[1][0].copy_(hA, non_blocking=True)
+        bufs[1][1].copy_(hB, non_blocking=True)
+    with torch.cuda.stream(d2h):
+        hC[0].copy_(bufs[1][2], non_blocking=True)
+    e1.record(h2d)
+    e2.record(d2h)
+    torch.cuda.synchronize()
+    both_ms = max(e0.elapsed_time(e1), e0.elapsed_time(e2))
     S = args.size
     return {"value": 2 * S ** 3 / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
             "steps": n, "h2d_ms_alone": h2d_ms, "d2h_ms_alone": d2h_ms,
+            "h2d_d2h_concurrent_ms": both_ms,
             "h2d_bytes_per_step": int(hA.numel() * 2 + hB.numel() * 2),
             "d2h_bytes_per_step": int(hC[0].numel() * hC[0].element_size()),
             "pipelined": "H2D(s+1) / GEMM(s) / D2H(s-1) on separate streams"}
@@ -760,11 +776,34 @@ def main_ours(args):
                             max(1, d["comm_bytes_per_gpu"]["total"])}
             return wl
         extra["workloads_3d"] = guarded("workloads_3d", w3d)
+
+        def pumma():
+            # configs[3]'s 2-D algorithm: SUMMA / PUMMA panels on the rectangular shape,
+            # where the decompose grid differs from Algorithm 1's (e.g. (4,1) vs (2,2))
+            mnk = (2 * args.size, args.size // 2, args.size // 2)
+            out = {"M": mnk[0], "N": mnk[1], "K": mnk[2]}
+            for mapping in ("decompose", "heuristic"):
+                ex, r = run_mapping(args, rank, world, local, mapping, mnk)
+                ex.close()
+                del ex
+                torch.cuda.empty_cache()
+                out[mapping] = {k: r[k] for k in ("grid", "ms_per_step", "tflops",
+                                                  "comm_bytes_per_gpu_max", "comm_bytes_total",
+                                                  "gemm_launches_per_step")}
+            out["speedup"] = out["decompose"]["tflops"] / out["heuristic"]["tflops"]
+            out["comm_ratio"] = (out["heuristic"]["comm_bytes_total"] /
+                                 max(1, out["decompose"]["comm_bytes_total"]))
+            return out
+        extra["pumma"] = guarded("pumma", pumma)
     if not args.no_cannon:
         cn = {}
         if world in (1, 4):  # q x q grids: configs[0] is Cannon fp32 N=1024 on 2x2
             cn["cannon_fp32_N1024"] = guarded(
                 "cannon_fp32", lambda: run_cannon(args, rank, world, 1024, 1, "fp32"))
+            # configs[0] is launch-latency bound: the same multiply replayed as a CUDA graph
+            cn["cannon_fp32_N1024_graph"] = guarded(
+                "cannon_fp32_graph",
+                lambda: run_cannon(args, rank, world, 1024, 1, "fp32", graph=True))
             cn["cannon_bf16"] = guarded(
                 "cannon_bf16", lambda: run_cannon(args, rank, world, args.size, 1, "bf16"))
         if world == 8:       # configs[2]: Solomonik 2.5D on 2x2x2
@@ -859,7 +898,8 @@ def main_ours(args):
         "e2e": None if e2e is None else {k: e2e[k] for k in
                                          ("value", "unit", "h2d_bytes_per_step",
                                           "d2h_bytes_per_step", "ms_per_step", "steps",
-                                          "h2d_ms_alone", "d2h_ms_alone", "pipelined")
+                                          "h2d_ms_alone", "d2h_ms_alone",
+                                          "h2d_d2h_concurrent_ms", "pipelined")
                                          if k in e2e},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak,

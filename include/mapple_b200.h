@@ -210,6 +210,22 @@ int pm_ipc_close(void* base);
 int pm_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
                     int64_t height, void* stream);
 
+/* Stream-ordered barrier among the box's GPUs through peer memory (no NCCL):
+ * each GPU pushes its next epoch (*epoch + 1, advanced on the device, so the
+ * barrier is CUDA-graph capturable) into peer_slot[q] = &flags_q[rank] with a
+ * system-scope release store and waits until my_flags[q] reaches it for every
+ * peer q (acquire).  Replaces the per-round 4-byte NCCL all-reduce of the
+ * Cannon / 2.5D shifts (the orderings the reference's algorithms need between
+ * rounds).  Flags and epoch start at zero and only grow. */
+#define PM_BARRIER_MAX_RANKS 16
+typedef struct pm_peer_barrier_view {
+  int32_t* my_flags;                         /* [world] local, pushed by peers   */
+  int32_t* peer_slot[PM_BARRIER_MAX_RANKS];  /* &peer q's my_flags[rank]         */
+  int32_t* epoch;                            /* local device counter             */
+  int32_t world, rank;
+} pm_peer_barrier_view;
+int pm_peer_barrier(const pm_peer_barrier_view* view, void* stream);
+
 /* One 5-point Jacobi sweep of this GPU's rectangle of a block-mapped grid
  * (the paper's stencil workload; ownership from the Mapple
  * block mapping, halo totals = surface_volume, commvol.py:94-96).  Neighbour

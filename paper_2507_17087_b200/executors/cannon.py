@@ -11,8 +11,8 @@ every layer).  Layer l runs Cannon steps t in [l q/c, (l+1) q/c): it first
 skews (A(i, (i+j+t0) mod q) and B((i+j+t0) mod q, j) are pulled from their
 holders), then alternates C += A*B with the Cannon shifts (A from the right
 neighbour, B from the neighbour below), each a copy-engine pull of the
-neighbour's current block over NVLink; a stream-ordered 4-byte NCCL
-all-reduce per round orders the shifts (no data goes through NCCL).  With
+neighbour's current block over NVLink; a stream-ordered barrier through peer
+memory (csrc/barrier.cu, no NCCL) per round orders the shifts.  With
 c > 1 every step's product is reduce-added straight into the layer that owns
 those rows of C (TMA `.add` over NVLink), i.e. the 2.5D reduction is fused into
 the GEMMs.  fp32 operands run on the TF32 tensor cores, bf16 on the bf16 path.
@@ -152,7 +152,9 @@ class MappedCannon:
         self.peers = PeerBuffers({"A0": self.A0, "B0": self.B0, "Acur0": self.A[0],
                                   "Acur1": self.A[1], "Bcur0": self.Bt[0], "Bcur1": self.Bt[1],
                                   "C0": self.C[0], "C1": self.C[1]}, rank, world, group)
-        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        from ..peer import PeerBarrier
+
+        self._bar = PeerBarrier(rank, world, group) if world > 1 else None
         self._dist = dist if world > 1 else None
         self.step_i = 0
         self.moved_blocks = 0
@@ -163,9 +165,10 @@ class MappedCannon:
         if self._dist:
             dist.barrier(group=group)
 
-    def _barrier(self):
-        if self._dist:
-            self._dist.all_reduce(self.flag, group=self.group)
+    def _barrier(self, stream=None):
+        """Stream-ordered all-GPU barrier through peer memory (no NCCL on the path)."""
+        if self._bar is not None:
+            self._bar(stream)
 
     def _pull(self, name, src_rank, dst_tensor, stream):
         from ..peer import copy2d
@@ -216,7 +219,7 @@ class MappedCannon:
         first = True  # the first local product overwrites C (Cannon); 2.5D always adds
         for op in cannon_schedule(q, c, self.coord):
             if op[0] == "barrier":
-                self._barrier()
+                self._barrier(cs)
             elif op[0] == "pull":
                 _, name, src, (kind, slot) = op
                 dst = self.A[slot] if kind == "A" else self.Bt[slot]
@@ -252,4 +255,6 @@ class MappedCannon:
         if self._graphs:
             native.require_cuda().cuda.synchronize()
             self._graphs.clear()
+        if self._bar is not None:
+            self._bar.close()
         self.peers.close()

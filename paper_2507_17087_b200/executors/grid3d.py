@@ -17,8 +17,9 @@ GPU (a, b, c) computes the partial product A[a, c] * B[c, b] over K block c:
     epilogue reduce-adds the tile straight into the owner's C buffer over
     NVLink (TMA `cp.reduce.async.bulk.tensor .add` on an IPC-mapped pointer) --
     the collective is fused into the GEMM, there is no separate NCCL call.
-C is double-buffered; one stream-ordered barrier per step (a 4-byte NCCL
-all-reduce) separates the zeroing of a buffer from the peers' adds into it.
+C is double-buffered; one stream-ordered barrier per step (through peer memory,
+csrc/barrier.cu -- no NCCL) separates the zeroing of a buffer from the peers'
+adds into it.
 """
 
 from __future__ import annotations
@@ -133,7 +134,9 @@ class MappedGemm3D:
         self.gemms = [(split(mb, pk, d), self.owner[(a, b, d)]) for d in order]
         self.done = torch.cuda.Event()
         self.done.record()
-        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        from ..peer import PeerBarrier
+
+        self._bar = PeerBarrier(rank, world, group) if world > 1 else None
         self.step_i = 0
         self.reduce = pk > 1
         self.flops = 2 * mb * nb * kb
@@ -147,8 +150,8 @@ class MappedGemm3D:
             dist.barrier(group=group)
 
     def _barrier(self):
-        if self._dist:  # stream-ordered: NCCL runs after the queued GEMMs
-            self._dist.all_reduce(self.flag, group=self.group)
+        if self._bar is not None:  # stream-ordered: runs after the queued GEMMs
+            self._bar()
 
     def step(self, stream=None):
         torch = native.require_cuda()
@@ -192,4 +195,6 @@ class MappedGemm3D:
         return self.C[(self.step_i - 1) % 2]
 
     def close(self):
+        if self._bar is not None:
+            self._bar.close()
         self.peers.close()

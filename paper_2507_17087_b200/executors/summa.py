@@ -173,11 +173,14 @@ def plan_panels(layout: Layout, me: int, K: int, mr: int, nc: int, block: int = 
     """The per-GPU SUMMA schedule (pure; CPU-testable).
 
     K is cut at every slice boundary of my row group (A) and column group (B),
-    so on each panel both operands come from single GPUs.  Panels whose
-    operands are both local run first -- no waiting -- while the copy engines
-    bring in the others; remote panels are split into row chunks of A so the
-    GEMM of chunk c overlaps the pull of chunk c+1.  The first panel writes C,
-    later ones accumulate (TMA reduce-add epilogue).
+    so on each panel both operands come from single GPUs.  The least-remote
+    panel (plus the fully local panels next to it in K) runs first -- no or
+    little waiting -- while the copy engines bring in the others; the remaining
+    panels merge with their K neighbours into runs (one launch per run and
+    A-row chunk: fewer accumulate passes over C, longer-K launches); runs that
+    pull A are split into row chunks of A so the GEMM of chunk c overlaps the
+    pull of chunk c+1.  The first run writes C, later ones accumulate (TMA
+    reduce-add epilogue).
     """
     cuts = {0, K}
     for q in layout.row_group[me]:
@@ -196,6 +199,26 @@ def plan_panels(layout: Layout, me: int, K: int, mr: int, nc: int, block: int = 
         remote = (a_src != me) * mr * (k1 - k0) + (b_src != me) * nc * (k1 - k0)
         ranked.append((remote, k0, k1, a_src, b_src))
     ranked.sort()
+    # runs: one GEMM per run and A-row chunk -- fewer accumulate passes over C and
+    # longer-K launches.  The first run is the least-remote panel (with the fully
+    # local panels K-adjacent to it, which cost no waiting); every other panel merges
+    # with its K neighbours, and those runs' pulls overlap the first run's GEMM.
+    head = [ranked[0]]
+    if ranked[0][0] == 0:
+        for r in sorted(ranked[1:], key=lambda r: r[1]):
+            if r[0] == 0 and r[1] == head[-1][2]:
+                head.append(r)
+        for r in sorted(ranked[1:], key=lambda r: -r[1]):
+            if r[0] == 0 and r[2] == head[0][1]:
+                head.insert(0, r)
+    runs = []
+    for r in sorted((r for r in ranked if r not in head), key=lambda r: r[1]):
+        if runs and runs[-1][-1][2] == r[1]:
+            runs[-1].append(r)
+        else:
+            runs.append([r])
+    runs.sort(key=lambda run: (sum(r[0] for r in run), run[0][1]))
+    runs.insert(0, head)
     nbr = -(-mr // block)
     n = max(1, min(a_chunks, nbr))
     chunks = [(min(mr, nbr * c // n * block), min(mr, nbr * (c + 1) // n * block))
@@ -218,13 +241,18 @@ def plan_panels(layout: Layout, me: int, K: int, mr: int, nc: int, block: int = 
         return idx
 
     first = True
-    for _, k0, k1, a_src, b_src in ranked:
-        b_evs = pull("Bt", b_src, 0, nc, k0, k1) if b_src != me else []
-        for r0, r1 in (chunks if a_src != me else [(0, mr)]):
-            a_evs = pull("A", a_src, r0, r1 - r0, k0, k1) if a_src != me else []
+    for run in runs:
+        k0, k1 = run[0][1], run[-1][2]
+        b_evs = [i for _, p0, p1, _, b_src in run if b_src != me
+                 for i in pull("Bt", b_src, 0, nc, p0, p1)]
+        a_remote = any(a_src != me for _, _, _, a_src, _ in run)
+        for r0, r1 in (chunks if a_remote else [(0, mr)]):
+            a_evs = [i for _, p0, p1, a_src, _ in run if a_src != me
+                     for i in pull("A", a_src, r0, r1 - r0, p0, p1)]
             gemms.append((r0, r1, k0, k1, not first, b_evs + a_evs))
-            b_evs = []  # later chunks of this panel run after the first on one stream
+            b_evs = []  # later chunks of this run follow the first on one stream
         first = False
+    ranked = [r for run in runs for r in run]
     return PanelPlan([(k0, k1, a, b) for _, k0, k1, a, b in ranked], chunks, pulls, gemms,
                      n_streams)
 

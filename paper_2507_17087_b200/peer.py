@@ -56,6 +56,42 @@ class PeerBuffers:
         self._opened = []
 
 
+class PmPeerBarrierView(ctypes.Structure):
+    _fields_ = [("my_flags", ctypes.c_void_p), ("peer_slot", ctypes.c_void_p * 16),
+                ("epoch", ctypes.c_void_p), ("world", ctypes.c_int32), ("rank", ctypes.c_int32)]
+
+
+class PeerBarrier:
+    """Stream-ordered barrier of the box's ranks through peer memory (csrc/barrier.cu):
+    a 32-thread kernel pushes the next epoch into every peer's flag slot and waits
+    for theirs -- no NCCL, and capturable in a CUDA graph (the epoch advances on
+    the device)."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        torch = native.require_cuda()
+        if world > 16:
+            raise ValueError("pm_peer_barrier supports up to 16 ranks")
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.flags = torch.zeros(max(world, 1), dtype=torch.int32, device=dev)
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize()  # zeroed before any peer can push into them
+        self.peers = PeerBuffers({"flags": self.flags}, rank, world, group)
+        v = PmPeerBarrierView()
+        v.my_flags = self.flags.data_ptr()
+        for q in range(world):
+            v.peer_slot[q] = self.peers.ptrs["flags"][q] + 4 * rank
+        v.epoch = self.epoch.data_ptr()
+        v.world, v.rank = world, rank
+        self.view = v
+
+    def __call__(self, stream=None) -> None:
+        native.check(native.lib().pm_peer_barrier(ctypes.byref(self.view),
+                                                  native.stream_ptr(stream)), "pm_peer_barrier")
+
+    def close(self):
+        self.peers.close()
+
+
 def copy2d(dst: int, dpitch: int, src: int, spitch: int, width: int, height: int, stream) -> None:
     """Pitched byte copy on the copy engines (peer or local), stream-ordered."""
     native.check(native.lib().pm_copy2d_async(dst, dpitch, src, spitch, width, height,
