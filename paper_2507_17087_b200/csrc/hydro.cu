@@ -77,13 +77,20 @@ k_hydro_zones(const __grid_constant__ HydroArgs a) {
   v.za[z] = area;
   v.zpe[z] = pe;
   // corner force of point k = half of each adjacent edge's pressure force, deposited
-  // with one 8-byte vector atomic (sm_90+ float2 atomicAdd) in the owner's memory
+  // in the owner's memory: one 8-byte vector atomic (sm_90+ float2 atomicAdd) into
+  // this GPU's points; two 4-byte float atomics -- the form NVLink peer atomics
+  // natively support -- into a peer's
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int km = (k + 3) & 3;
     const int r = rk(ref[k]), s = sl(ref[k]);
-    atomicAdd(reinterpret_cast<float2*>(v.fxy[r]) + s,
-              make_float2(0.5f * pe * (nx[km] + nx[k]), 0.5f * pe * (ny[km] + ny[k])));
+    const float fx = 0.5f * pe * (nx[km] + nx[k]), fy = 0.5f * pe * (ny[km] + ny[k]);
+    if (r == v.rank) {
+      atomicAdd(reinterpret_cast<float2*>(v.fxy[r]) + s, make_float2(fx, fy));
+    } else {
+      atomicAdd(v.fxy[r] + 2 * s, fx);
+      atomicAdd(v.fxy[r] + 2 * s + 1, fy);
+    }
   }
 }
 

@@ -186,25 +186,28 @@ class MappedCircuit:
             v.charge[r] = self.peers.ptrs["charge"][r]
         v.rank, v.steps, v.dt = rank, spec.steps, spec.dt
         self.view = v
-        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        from ..peer import PeerBarrier
+
+        self._bar = PeerBarrier(rank, world, group) if world > 1 else None
         self._dist = dist if world > 1 else None
         self.iterations = 0
         torch.cuda.synchronize()
         if self._dist:
             dist.barrier(group=group)
 
-    def _barrier(self):
-        if self._dist:
-            self._dist.all_reduce(self.flag, group=self.group)
+    def _barrier(self, stream=None):
+        """Stream-ordered all-GPU barrier through peer memory (csrc/barrier.cu)."""
+        if self._bar is not None:
+            self._bar(stream)
 
     def step(self, stream=None):
         """One iteration: calc_new_currents + distribute_charge, update_voltages."""
         torch = native.require_cuda()
         lib = native.lib()
         cs = native.stream_ptr(stream or torch.cuda.current_stream())
-        self._barrier()  # every GPU's voltages are final
+        self._barrier(stream)  # every GPU's voltages are final
         native.check(lib.pm_circuit_step(ctypes.byref(self.view), 0, cs), "pm_circuit_step")
-        self._barrier()  # every GPU's charge deposits have landed
+        self._barrier(stream)  # every GPU's charge deposits have landed
         native.check(lib.pm_circuit_step(ctypes.byref(self.view), 1, cs), "pm_circuit_step")
         self.iterations += 1
 
@@ -220,4 +223,6 @@ class MappedCircuit:
                 "nvlink_bytes_per_iteration": 8 * self.cross_gpu_wires}
 
     def close(self):
+        if self._bar is not None:
+            self._bar.close()
         self.peers.close()

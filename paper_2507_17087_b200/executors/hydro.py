@@ -135,24 +135,27 @@ class MappedHydro:
                 arr[r] = self.peers.ptrs[n][r]
         v.rank, v.dt, v.gamma, v.cq = rank, hydro_dt(spec), spec.gamma, spec.cq
         self.view = v
-        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        from ..peer import PeerBarrier
+
+        self._bar = PeerBarrier(rank, world, group) if world > 1 else None
         self._dist = dist if world > 1 else None
         torch.cuda.synchronize()
         if self._dist:
             dist.barrier(group=group)
 
-    def _barrier(self):
-        if self._dist:
-            self._dist.all_reduce(self.flag, group=self.group)
+    def _barrier(self, stream=None):
+        """Stream-ordered all-GPU barrier through peer memory (csrc/barrier.cu)."""
+        if self._bar is not None:
+            self._bar(stream)
 
     def step(self, stream=None):
         """One Lagrangian step: zones (forces to points), then points (kinematics)."""
         torch = native.require_cuda()
         lib = native.lib()
         cs = native.stream_ptr(stream or torch.cuda.current_stream())
-        self._barrier()  # all points moved
+        self._barrier(stream)  # all points moved
         native.check(lib.pm_hydro_step(ctypes.byref(self.view), 0, cs), "pm_hydro_step")
-        self._barrier()  # all corner forces deposited
+        self._barrier(stream)  # all corner forces deposited
         native.check(lib.pm_hydro_step(ctypes.byref(self.view), 1, cs), "pm_hydro_step")
 
     # algorithmic HBM bytes per zone-step: zone kernel 16 (z2p) + 16 (zm, ze, za, zpe) +
@@ -160,4 +163,6 @@ class MappedHydro:
     BYTES_PER_ZONE_STEP = 16 + 16 + 12 + 16 + 8 + 29 + 24
 
     def close(self):
+        if self._bar is not None:
+            self._bar.close()
         self.peers.close()

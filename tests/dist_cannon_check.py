@@ -24,10 +24,15 @@ def main():
 
     faulthandler.dump_traceback_later(int(os.environ.get("PM_HANG_DUMP_S", "240")), exit=False)
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # PM_TEST_BACKEND=gloo: host collectives over gloo, so more ranks than GPUs can
+    # share the box (rank r on GPU r % n; peers on the same GPU through CUDA IPC) --
+    # exercises the 8-GPU paths on a 4-GPU box; the executors' data path has no NCCL
+    backend = os.environ.get("PM_TEST_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group(backend, **({"device_id": torch.device("cuda", local)}
+                                            if backend == "nccl" else {}))
     out = []
     configs = []
     for c in (1, 2, 4, 8):

@@ -25,10 +25,15 @@ TOL = 1e-4  # fp32 arithmetic vs float64, a few iterations
 
 def main():
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # PM_TEST_BACKEND=gloo: host collectives over gloo, so more ranks than GPUs can
+    # share the box (rank r on GPU r % n; peers on the same GPU through CUDA IPC) --
+    # exercises the 8-GPU paths on a 4-GPU box; the executors' data path has no NCCL
+    backend = os.environ.get("PM_TEST_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group(backend, **({"device_id": torch.device("cuda", local)}
+                                            if backend == "nccl" else {}))
     res = []
     for spec, iters in ((CircuitSpec(12, 64, 256, pct_in=80, steps=20, seed=3), 4),
                         (CircuitSpec(5, 33, 100, pct_in=50, steps=7, seed=1), 3)):

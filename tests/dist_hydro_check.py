@@ -24,16 +24,24 @@ from paper_2507_17087_b200.factorize import greedy_grid  # noqa: E402
 TOL = 1e-3  # fp32 vs float64 after 20 steps, errors normalised by the field's max
 
 
-def rel(a, b):
-    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30)) if a.size else 0.0
+def rel(a, b, full):
+    """Max error normalised by the field's max over the WHOLE mesh (`full`), not over
+    this rank's share: an 8-way split leaves ranks whose points barely move, and their
+    own max made f32 rounding look like 1e-2 errors."""
+    return float(np.abs(a - b).max() / max(np.abs(full).max(), 1e-30)) if a.size else 0.0
 
 
 def main():
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # PM_TEST_BACKEND=gloo: host collectives over gloo, so more ranks than GPUs can
+    # share the box (rank r on GPU r % n; peers on the same GPU through CUDA IPC) --
+    # exercises the 8-GPU paths on a 4-GPU box; the executors' data path has no NCCL
+    backend = os.environ.get("PM_TEST_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group(backend, **({"device_id": torch.device("cuda", local)}
+                                            if backend == "nccl" else {}))
     res = []
     steps = 20
     for Lx, Ly in ((48, 40), (37, 29)):
@@ -49,9 +57,9 @@ def main():
             pid = ex.point_ids.cpu().numpy()
             zid = ex.zone_ids.cpu().numpy()
             n = pid.size
-            errs = {k: rel(getattr(ex, a)[:n].double().cpu().numpy(), ref[k][pid])
+            errs = {k: rel(getattr(ex, a)[:n].double().cpu().numpy(), ref[k][pid], ref[k])
                     for k, a in (("x", "px"), ("y", "py"), ("u", "ux"), ("v", "uy"))}
-            errs["e"] = rel(ex.ze.double().cpu().numpy(), ref["e"][zid])
+            errs["e"] = rel(ex.ze.double().cpu().numpy(), ref["e"][zid], ref["e"])
             # owners and the exchange model from the oracle's mapping
             g0 = greedy_grid(world, 2)[0]
             zo = np.asarray(O.map_launch(parse(STENCIL_MAPPERS.format(g0=g0)),

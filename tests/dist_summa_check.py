@@ -26,9 +26,14 @@ from paper_2507_17087_b200.factorize import greedy_grid  # noqa: E402
 
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # PM_TEST_BACKEND=gloo: host collectives over gloo, so more ranks than GPUs can
+    # share the box (rank r on GPU r % n; peers on the same GPU through CUDA IPC) --
+    # exercises the 8-GPU paths on a 4-GPU box; the executors' data path has no NCCL
+    backend = os.environ.get("PM_TEST_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist.init_process_group(backend, **({"device_id": torch.device("cuda", local)}
+                                            if backend == "nccl" else {}))
     results = []
     for (M, N, K) in [(2048, 2048, 2048), (4096, 2048, 1024), (1536, 2560, 768)]:
         for mapping in ("decompose", "heuristic"):

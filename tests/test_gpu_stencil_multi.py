@@ -83,3 +83,27 @@ def test_hydro(n):
         pytest.skip(f"needs {n} GPUs")
     v = _run("dist_hydro_check.py", n, 29790 + n)
     assert v["ok"], v
+
+
+EIGHT = ["cannon", "grid3d", "summa", "stencil", "circuit", "hydro"]
+
+
+@pytest.mark.parametrize("script", EIGHT)
+def test_eight_ranks_on_fewer_gpus(script):
+    """The N=8 paths (Solomonik 2.5D with c=2, 2x2x2 / (2,4) / (4,2) grids, 8-way
+    stencil / circuit / hydro) with 8 ranks sharing the box's GPUs: host collectives
+    over gloo, peers on the same GPU through CUDA IPC (the executors' data path and
+    barriers use peer memory only, no NCCL)."""
+    import os
+
+    n = _ngpus()
+    if n < 2:
+        pytest.skip("needs 2+ GPUs")
+    env = dict(os.environ, PM_TEST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr", "127.0.0.1", "--master-port", str(29810 + EIGHT.index(script)),
+           str(ROOT / "tests" / f"dist_{script}_check.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-4000:]
+    v = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert v["ok"] and v["world"] == 8, v
