@@ -411,9 +411,10 @@ k_halo2d_count(Strip2D h, int npairs, long long* __restrict__ tile_cnt,
                unsigned short* __restrict__ warp_pre) {
   extern __shared__ int sp[];  // [npairs]
   __shared__ int s_row[kStripRows][kPartWarps];
-  __shared__ int s_any;
+  __shared__ unsigned s_mask[kStripRows / 32][kPartWarps];
+  __shared__ int s_any, s_done;
   for (int b = threadIdx.x; b < npairs; b += kPartThreads) sp[b] = 0;
-  if (threadIdx.x == 0) s_any = 0;
+  if (threadIdx.x == 0) s_any = 0, s_done = 0;
   __syncthreads();
   const int seg = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long r0 = (long long)blockIdx.y * kStripRows;
@@ -435,34 +436,53 @@ k_halo2d_count(Strip2D h, int npairs, long long* __restrict__ tile_cnt,
     if (lane == 0) s_row[i][warp] = tot;
   });
   if (any) s_any = 1;
-  __syncthreads();
-  if (threadIdx.x < nr) {
-    int c = 0;
-#pragma unroll
-    for (int w = 0; w < kPartWarps; ++w) c += s_row[threadIdx.x][w];
-    tile_cnt[(r0 + threadIdx.x) * h.nseg + seg] = c;
-  }
-  // per warp: which of the block's rows hold its entries (the compaction skips the
-  // rest) and, in non-empty tiles, its first entry within the tile (<= 4 * kStripCells)
-  unsigned long long rows_hit = 0;
+  // the last warp to finish does the block's epilogue; the others leave at once (a
+  // block-wide barrier here kept 7 warps waiting for the slowest one)
+  __threadfence_block();
+  int last = 0;
+  if (lane == 0) last = atomicAdd(&s_done, 1) == kPartWarps - 1;
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  __threadfence_block();
+  // per tile (row): its entry count; per warp: which rows hold its entries (the
+  // compaction skips the rest) and, in non-empty tiles, its first entry within the tile
+  const long long blk = (long long)blockIdx.y * h.nseg + seg;
 #pragma unroll
   for (int q = 0; q < kStripRows / 32; ++q) {
     const int i = 32 * q + lane;
-    int before = 0, all = 0;
-    if (i < nr) {
+    int c[kPartWarps];
+    int all = 0;
 #pragma unroll
-      for (int v = 0; v < kPartWarps; ++v) {
-        const int x = s_row[i][v];
-        before += v < warp ? x : 0;
-        all += x;
-      }
-      if (all) warp_pre[((r0 + i) * h.nseg + seg) * kPartWarps + warp] = (unsigned short)before;
+    for (int w = 0; w < kPartWarps; ++w) {
+      c[w] = i < nr ? s_row[i][w] : 0;
+      all += c[w];
     }
-    rows_hit |= (unsigned long long)__ballot_sync(0xffffffffu, i < nr && s_row[i < nr ? i : 0][warp]) << (32 * q);
+    if (i < nr) {
+      tile_cnt[(r0 + i) * h.nseg + seg] = all;
+      if (all) {
+        int before = 0;
+#pragma unroll
+        for (int w = 0; w < kPartWarps; ++w) {
+          warp_pre[((r0 + i) * h.nseg + seg) * kPartWarps + w] = (unsigned short)before;
+          before += c[w];
+        }
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < kPartWarps; ++w) {
+      const unsigned m = __ballot_sync(0xffffffffu, c[w] != 0);
+      if (lane == w) s_mask[q][w] = m;
+    }
   }
-  if (lane == 0) warp_rows[((long long)blockIdx.y * h.nseg + seg) * kPartWarps + warp] = rows_hit;
+  __syncwarp();
+  if (lane < kPartWarps) {
+    unsigned long long rows_hit = 0;
+#pragma unroll
+    for (int q = 0; q < kStripRows / 32; ++q)
+      rows_hit |= (unsigned long long)s_mask[q][lane] << (32 * q);
+    warp_rows[blk * kPartWarps + lane] = rows_hit;
+  }
   if (s_any)
-    for (int b = threadIdx.x; b < npairs; b += kPartThreads)
+    for (int b = lane; b < npairs; b += 32)
       if (sp[b]) atomicAdd(pair_cnt + b, (unsigned long long)sp[b]);
 }
 
