@@ -592,6 +592,7 @@ def cpu_sample(args, threads=None):
     dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
     A = synth((0, r), (0, S), S, 1234, dev).float().cpu().numpy().astype(np.float64)
     Bt = synth((0, c), (0, S), S, 1235, dev).float().cpu().numpy().astype(np.float64)
+    lim, used = blas_threads()
     # repeat the bounded sample until ~10 s of host work (contract: 10-30 s)
     t = time.perf_counter()
     C = sample_rows_cols(A, Bt)
@@ -600,7 +601,7 @@ def cpu_sample(args, threads=None):
         sample_rows_cols(A, Bt)
         reps += 1
     dt = (time.perf_counter() - t) / reps
-    return C, dt, 2.0 * r * c * S
+    return C, dt, 2.0 * r * c * S, used
 
 
 def run_sharded_mapping(args, rank, world):
@@ -840,8 +841,8 @@ def main_ours(args):
         extra["pennant_hydro"] = guarded("pennant_hydro", hydro)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        C64, dt, fl = cpu_sample(args)
-        cpu = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": len(os.sched_getaffinity(0)),
+        C64, dt, fl, used = cpu_sample(args)
+        cpu = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": used,
                "kind": "port",
                "sample": f"numpy float64 C[0:{args.cpu_rows}, 0:{args.cpu_cols}] of the "
                          f"{args.size}^3 product (full K), {dt:.2f} s each, repeated for "
@@ -931,6 +932,18 @@ def main_ours(args):
     print(json.dumps(line), flush=True)
 
 
+def blas_threads():
+    """Every host core of the affinity mask for numpy's BLAS, whatever OMP_NUM_THREADS
+    torchrun set (it pins each rank to 1 thread); returns (limiter, threads in use)."""
+    from threadpoolctl import threadpool_info, threadpool_limits
+
+    cores = len(os.sched_getaffinity(0))
+    lim = threadpool_limits(limits=cores, user_api="blas")
+    used = max([p.get("num_threads", 1) for p in threadpool_info()
+                if p.get("user_api") == "blas"] or [1])
+    return lim, used
+
+
 def main_reference(args):
     """Reference arm: the CPU path (oracle port) on the host cores, rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
@@ -940,6 +953,7 @@ def main_reference(args):
 
     from oracle.numerics import sample_rows_cols
 
+    lim, cores = blas_threads()
     S = args.size
     r, c = args.cpu_rows, args.cpu_cols
     rng = np.random.default_rng(1234)
@@ -958,7 +972,7 @@ def main_reference(args):
         times.append((time.perf_counter() - t) / reps)
     dt = statistics.mean(times)
     v = 2.0 * r * c * S / dt / 1e12
-    cores = len(os.sched_getaffinity(0))
+    lim.unregister() if hasattr(lim, "unregister") else None
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s",
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": len(times),
