@@ -225,6 +225,18 @@ typedef struct pm_peer_barrier_view {
   int32_t world, rank;
 } pm_peer_barrier_view;
 int pm_peer_barrier(const pm_peer_barrier_view* view, void* stream);
+/* Up to PM_PEER_COPY_MAX contiguous copies (peer or local, 16-byte aligned, bytes a
+ * multiple of 16) done by the SMs, then the same barrier, in one launch: a Cannon /
+ * 2.5D shift round when its blocks are small and the round latency-bound.  `ticket`:
+ * a device uint32, zero at first use (the kernel leaves it zero). */
+#define PM_PEER_COPY_MAX 4
+typedef struct pm_peer_copy {
+  void* dst;
+  const void* src;
+  int64_t bytes;
+} pm_peer_copy;
+int pm_peer_copy_barrier(const pm_peer_barrier_view* view, const pm_peer_copy* copies,
+                         int32_t n, uint32_t* ticket, void* stream);
 
 /* One 5-point Jacobi sweep of this GPU's rectangle of a block-mapped grid
  * (the paper's stencil workload; ownership from the Mapple

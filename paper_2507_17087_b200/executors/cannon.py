@@ -155,6 +155,9 @@ class MappedCannon:
         from ..peer import PeerBarrier
 
         self._bar = PeerBarrier(rank, world, group) if world > 1 else None
+        # small blocks: the SMs copy a round's blocks and run its barrier in one launch
+        # (latency-bound rounds, configs[0]); large ones go to the copy engines
+        self._fused_pulls = nb * nb * (4 if dtype == "fp32" else 2) <= (8 << 20)
         self._dist = dist if world > 1 else None
         self.step_i = 0
         self.moved_blocks = 0
@@ -169,15 +172,6 @@ class MappedCannon:
         """Stream-ordered all-GPU barrier through peer memory (no NCCL on the path)."""
         if self._bar is not None:
             self._bar(stream)
-
-    def _pull(self, name, src_rank, dst_tensor, stream):
-        from ..peer import copy2d
-
-        pitch = self.nb * dst_tensor.element_size()
-        src = self.peers.ptrs[name][src_rank]
-        if src_rank == self.rank:
-            src = self.peers.ptrs[name][self.rank]
-        copy2d(dst_tensor.data_ptr(), pitch, src, pitch, pitch, self.nb, stream)
 
     def step(self, stream=None):
         """One full multiply (all Cannon / 2.5D steps and the layer reduction).
@@ -217,13 +211,23 @@ class MappedCannon:
             self.C[buf].zero_()
         moved = 0
         first = True  # the first local product overwrites C (Cannon); 2.5D always adds
+        pending = []  # a round's pulls, issued with its closing barrier (one launch)
         for op in cannon_schedule(q, c, self.coord):
             if op[0] == "barrier":
-                self._barrier(cs)
+                if self._bar is not None and pending and self._fused_pulls:
+                    self._bar.copy_then_wait([(d, sp, w * h) for d, sp, w, h in pending], cs)
+                else:
+                    from ..peer import copy2d
+
+                    for d, sp, w, h in pending:  # copy engines, pitched rows
+                        copy2d(d, w, sp, w, w, h, cs)
+                    self._barrier(cs)
+                pending = []
             elif op[0] == "pull":
                 _, name, src, (kind, slot) = op
                 dst = self.A[slot] if kind == "A" else self.Bt[slot]
-                self._pull(name, self.owner[src], dst, cs)
+                pending.append((dst.data_ptr(), self.peers.ptrs[name][self.owner[src]],
+                                self.nb * dst.element_size(), self.nb))
                 moved += self.owner[src] != self.rank
             else:  # C(rows of layer d) += A(i,k) B(k,j), reduce-added into the owning layer
                 _, slot, d = op

@@ -120,6 +120,8 @@ def stream_ptr(stream=None) -> int:
 
 SIGNATURES["pm_stencil_sweep"] = (ctypes.c_int, [ctypes.c_void_p, _I32, _VP])
 SIGNATURES["pm_peer_barrier"] = (ctypes.c_int, [ctypes.c_void_p, _VP])
+SIGNATURES["pm_peer_copy_barrier"] = (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _I32,
+                                                     _VP, _VP])
 SIGNATURES["pm_circuit_step"] = (ctypes.c_int, [ctypes.c_void_p, _I32, _VP])
 SIGNATURES["pm_hydro_step"] = (ctypes.c_int, [ctypes.c_void_p, _I32, _VP])
 SIGNATURES["pm_map_partition_scratch_bytes"] = (ctypes.c_size_t, [_I64, _I32])

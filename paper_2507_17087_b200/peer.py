@@ -61,6 +61,10 @@ class PmPeerBarrierView(ctypes.Structure):
                 ("epoch", ctypes.c_void_p), ("world", ctypes.c_int32), ("rank", ctypes.c_int32)]
 
 
+class PmPeerCopy(ctypes.Structure):
+    _fields_ = [("dst", ctypes.c_void_p), ("src", ctypes.c_void_p), ("bytes", ctypes.c_int64)]
+
+
 class PeerBarrier:
     """Stream-ordered barrier of the box's ranks through peer memory (csrc/barrier.cu):
     a 32-thread kernel pushes the next epoch into every peer's flag slot and waits
@@ -74,6 +78,7 @@ class PeerBarrier:
         dev = torch.device("cuda", torch.cuda.current_device())
         self.flags = torch.zeros(max(world, 1), dtype=torch.int32, device=dev)
         self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
         torch.cuda.synchronize()  # zeroed before any peer can push into them
         self.peers = PeerBuffers({"flags": self.flags}, rank, world, group)
         v = PmPeerBarrierView()
@@ -87,6 +92,17 @@ class PeerBarrier:
     def __call__(self, stream=None) -> None:
         native.check(native.lib().pm_peer_barrier(ctypes.byref(self.view),
                                                   native.stream_ptr(stream)), "pm_peer_barrier")
+
+    def copy_then_wait(self, copies, stream=None) -> None:
+        """[(dst_ptr, src_ptr, bytes)] copied by the SMs (peer or local), then this
+        barrier -- one launch (pm_peer_copy_barrier)."""
+        if len(copies) > 4:
+            raise ValueError("at most 4 copies per launch")
+        arr = (PmPeerCopy * max(1, len(copies)))(*[PmPeerCopy(d, s, n) for d, s, n in copies])
+        native.check(native.lib().pm_peer_copy_barrier(ctypes.byref(self.view), arr, len(copies),
+                                                       self.ticket.data_ptr(),
+                                                       native.stream_ptr(stream)),
+                     "pm_peer_copy_barrier")
 
     def close(self):
         self.peers.close()
