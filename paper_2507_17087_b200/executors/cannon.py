@@ -225,6 +225,8 @@ class MappedCannon:
                 pending = []
             elif op[0] == "pull":
                 _, name, src, (kind, slot) = op
+                if q == 1:  # a 1x1 grid has no shifts: multiply the own blocks in place
+                    continue
                 dst = self.A[slot] if kind == "A" else self.Bt[slot]
                 pending.append((dst.data_ptr(), self.peers.ptrs[name][self.owner[src]],
                                 self.nb * dst.element_size(), self.nb))
@@ -233,15 +235,16 @@ class MappedCannon:
                 _, slot, d = op
                 r0, r1 = split(self.nb, c, d)
                 cptr = self.peers.ptrs[f"C{buf}"][self.owner[(i, j, d)]]
-                a = self.A[slot][r0:r1]
+                a_blk, b_blk = (self.A0, self.B0) if q == 1 else (self.A[slot], self.Bt[slot])
+                a = a_blk[r0:r1]
                 acc = 2 if c > 1 else int(not first)
                 if self.dtype == "fp32":
-                    native.check(lib.pm_gemm_tf32(a.data_ptr(), self.nb, self.Bt[slot].data_ptr(),
+                    native.check(lib.pm_gemm_tf32(a.data_ptr(), self.nb, b_blk.data_ptr(),
                                                   self.nb, cptr, self.nb, r1 - r0, self.nb,
                                                   self.nb, acc, native.stream_ptr(cs)),
                                  "pm_gemm_tf32")
                 else:
-                    native.check(lib.pm_gemm_bf16(a.data_ptr(), self.nb, self.Bt[slot].data_ptr(),
+                    native.check(lib.pm_gemm_bf16(a.data_ptr(), self.nb, b_blk.data_ptr(),
                                                   self.nb, cptr, self.nb, r1 - r0, self.nb,
                                                   self.nb, 0, acc, native.stream_ptr(cs)),
                                  "pm_gemm_bf16")
