@@ -170,6 +170,8 @@ struct Params {
   int debug_nostore;  // experiments only (PM_GEMM_NOSTORE): skip the C stores
   int tma_store;      // epilogue through smem + TMA bulk store (map_c valid)
   int* tile_counter;  // dynamic tile scheduler ticket (zeroed before each launch)
+  int k_split;        // 1-SM kernel: K slices per output tile (<= 1: none); > 1 adds
+                      // every slice's partial product into C with vector red.add
 };
 
 __device__ __forceinline__ void tile_coords(int t, const Params& p, int& tm, int& tn) {
@@ -204,7 +206,9 @@ k_gemm_1sm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CU
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int ntiles = p.tiles_m * p.tiles_n;
+  const int ksplit = p.k_split > 1 ? p.k_split : 1;
+  const int kb_per = (p.k_blocks + ksplit - 1) / ksplit;  // k-blocks per slice
+  const int ntiles = p.tiles_m * p.tiles_n * ksplit;      // (output tile, K slice) items
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
@@ -238,8 +242,9 @@ k_gemm_1sm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CU
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         int tm, tn;
-        tile_coords(t, p, tm, tn);
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        tile_coords(t / ksplit, p, tm, tn);
+        const int kb0 = (t % ksplit) * kb_per, kb1 = min(p.k_blocks, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           tma_load_2d(&map_a, &full[stage], sa + stage * A_BYTES, kb * BKE, tm * BM);
@@ -260,7 +265,8 @@ k_gemm_1sm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CU
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        const int kb0 = (t % ksplit) * kb_per, kb1 = min(p.k_blocks, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sa + stage * A_BYTES);
@@ -270,9 +276,9 @@ k_gemm_1sm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CU
             const uint64_t ad = smem_desc_sw128(a0 + k * UMMA_K * 2);
             const uint64_t bd = smem_desc_sw128(b0 + k * UMMA_K * 2);
             if constexpr (TF32)
-              tc_mma_tf32(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              tc_mma_tf32(d_tmem, ad, bd, idesc, ((kb - kb0) | k) != 0);
             else
-              tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              tc_mma(d_tmem, ad, bd, idesc, ((kb - kb0) | k) != 0);
           }
           tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -285,7 +291,7 @@ k_gemm_1sm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CU
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       int tm, tn;
-      tile_coords(t, p, tm, tn);
+      tile_coords(t / ksplit, p, tm, tn);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -301,7 +307,19 @@ k_gemm_1sm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CU
         const bool full_cols = col0 + 32 <= p.N;
         if (p.c32) {
           float* dst = p.c32 + (long long)row * p.ldc + col0;
-          if (full_cols && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+          if (ksplit > 1) {  // slices of one tile add concurrently: vector reduction-adds
+            if (full_cols && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + j),
+                             "f"(__uint_as_float(v[j])), "f"(__uint_as_float(v[j + 1])),
+                             "f"(__uint_as_float(v[j + 2])), "f"(__uint_as_float(v[j + 3]))
+                             : "memory");
+            } else {
+              for (int j = 0; j < 32 && col0 + j < p.N; ++j)
+                atomicAdd(dst + j, __uint_as_float(v[j]));
+            }
+          } else if (full_cols && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
               float4 o = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
@@ -1067,8 +1085,24 @@ extern "C" int pm_gemm_tf32(const float* A, int64_t lda, const float* Bt, int64_
                                      SMEM_BYTES));
     attr_done[dev] = true;
   }
-  const long long ntiles = (long long)p.tiles_m * p.tiles_n;
-  int grid = pm::num_sms();
+  const long long tiles = (long long)p.tiles_m * p.tiles_n;
+  // few output tiles (small products, e.g. Cannon's 512^3 blocks): split K over the idle
+  // SMs, every slice reduction-adding into C (zeroed first unless accumulating)
+  const int sms = pm::num_sms();
+  int ks = 1;
+  if (tiles * 2 <= sms && p.k_blocks >= 8) {
+    ks = (int)std::min<long long>(sms / tiles, p.k_blocks / 4);
+    const int kb_per = (p.k_blocks + ks - 1) / ks;
+    ks = (p.k_blocks + kb_per - 1) / kb_per;  // no empty slice
+  }
+  if (ks > 1) {
+    p.k_split = ks;
+    if (!p.accumulate)
+      PM_CUDA_TRY(cudaMemset2DAsync(C, ldc * sizeof(float), 0, N * sizeof(float), M,
+                                    (cudaStream_t)stream));
+  }
+  const long long ntiles = tiles * ks;
+  int grid = sms;
   if (ntiles < grid) grid = (int)ntiles;
   k_gemm_1sm<true><<<grid, kThreads, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, p);
   PM_CUDA_TRY(cudaGetLastError());

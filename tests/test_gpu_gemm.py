@@ -62,7 +62,8 @@ def test_gemm_strided_views(cuda):
     assert _rel(C, _ref(A, Bt)) < 1e-4
 
 
-@pytest.mark.parametrize("M,N,K", [(512, 512, 512), (1000, 700, 320), (128, 256, 32), (2048, 1024, 4096)])
+@pytest.mark.parametrize("M,N,K", [(512, 512, 512), (1000, 700, 320), (128, 256, 32), (2048, 1024, 4096),
+                                   (512, 384, 1000)])
 def test_tf32_gemm(cuda, M, N, K):
     from paper_2507_17087_b200.gemm import tile_gemm_tf32
 
