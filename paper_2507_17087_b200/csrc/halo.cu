@@ -486,14 +486,17 @@ k_halo2d_count(Strip2D h, int npairs, long long* __restrict__ tile_cnt,
       if (sp[b]) atomicAdd(pair_cnt + b, (unsigned long long)sp[b]);
 }
 
-__global__ void __launch_bounds__(kPartThreads, 3)
+__global__ void __launch_bounds__(32)
 k_halo2d_compact(Strip2D h, const long long* __restrict__ tile_off,
                  const unsigned long long* __restrict__ warp_rows,
                  const unsigned short* __restrict__ warp_pre, int* __restrict__ out_key,
                  long long* __restrict__ out_slot) {
-  const int seg = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // one warp per CTA (x = strip * 8 + warp of the count pass): only the few warps holding
+  // entries stay resident, instead of 256-thread CTAs pinned by their one busy warp
+  const int seg = blockIdx.x / kPartWarps, warp = blockIdx.x % kPartWarps;
+  const int lane = threadIdx.x & 31;
   const unsigned long long mine = warp_rows[((long long)blockIdx.y * h.nseg + seg) * kPartWarps + warp];
-  if (!mine) return;  // warp-uniform; no block-wide barrier below
+  if (!mine) return;
   const long long r0 = (long long)blockIdx.y * kStripRows;
   const int nr = (int)min((long long)kStripRows, h.rows - r0);
   // lane i: first output slot of this warp's entries in rows r0 + i and r0 + 32 + i
@@ -504,7 +507,7 @@ k_halo2d_compact(Strip2D h, const long long* __restrict__ tile_off,
       const long long t = (r0 + 32 * q + lane) * h.nseg + seg;
       first[q] = tile_off[t] + warp_pre[t * kPartWarps + warp];
     }
-  const long long c0 = (long long)seg * kStripCells + 4 * threadIdx.x;
+  const long long c0 = (long long)seg * kStripCells + 4 * (warp * 32 + lane);
   const bool active = c0 < h.cols;
   strip_rows(h, r0, nr, c0, [&](int i, const int4& up, const int4& cur, const int4& dn, int lf,
                                 int rt) {
@@ -706,9 +709,10 @@ int pm_halo_compact(const int32_t* owner, const int64_t* ext, int32_t rank, cons
   pm::Strip2D h2;
   if (pm::make_strip2d(owner, ext, rank, halo, nprocs, &h2)) {
     const long long* tile = reinterpret_cast<const long long*>(tile_scratch);
-    // warps without entries return after reading their row mask
-    const dim3 grid((unsigned)h2.nseg, (unsigned)((h2.rows + pm::kStripRows - 1) / pm::kStripRows));
-    pm::k_halo2d_compact<<<grid, pm::kPartThreads, 0, (cudaStream_t)stream>>>(
+    // one warp per CTA; warps without entries return after reading their row mask
+    const dim3 grid((unsigned)(h2.nseg * pm::kPartWarps),
+                    (unsigned)((h2.rows + pm::kStripRows - 1) / pm::kStripRows));
+    pm::k_halo2d_compact<<<grid, 32, 0, (cudaStream_t)stream>>>(
         h2, tile, pm::strip_warp_rows(h2, tile_scratch), pm::strip_warp_pre(h2, tile_scratch),
         keys, so);
     PM_CUDA_TRY(cudaGetLastError());
