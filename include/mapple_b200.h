@@ -112,6 +112,24 @@ void pm_plan_destroy(pm_plan* plan);
 int pm_map_batch(const pm_plan* plan, const int32_t* points, int64_t n, int64_t first,
                  int32_t* out_proc, uint64_t* status, void* stream);
 
+/* Failure probe for exact error messages
+ *   <- the reference formats the operand values into the message of the
+ *      exception it raises at the failing point ("index (3, 8) out of range for
+ *      shape (2, 2)", spaces.py:215-221 re-wrapped at dsl/interp.py:255-258;
+ *      "index 5 out of range for tuple of rank 2", dsl/interp.py:212-213;
+ *      "dimension 3 out of range for rank 2", dsl/interp.py:247-248).
+ * Re-evaluates the single point `index` (a launch index as reported in the
+ * status word: implicit mode = row-major linear index; explicit mode = the row
+ * of `points`) with a diagnostic twin of the plan's kernel, compiled on first
+ * use.  Device outputs: site[0] = the failing site (-1 if the point maps),
+ * site[1] = the result; dump[2 r], dump[2 r + 1] = register r at the failure as
+ * the low / high 64-bit words of its sign-extended 128-bit value, for
+ * r < pm_plan_regs(plan). */
+int pm_plan_regs(const pm_plan* plan);
+int pm_compile_check_probe(const pm_program* prog);  /* NVRTC build of the probe (no GPU) */
+int pm_map_probe(pm_plan* plan, const int32_t* points, int64_t index, int64_t* dump,
+                 int32_t* site, void* stream);
+
 /* Fused map + partition (K1 + K2 without materialising the processor ids)
  *   <- cmd_map's loop (cli.py:149-170) feeding expand_shards / shard_policy
  *      (tasksim/sim.py:67-120): the stable partition of launch points

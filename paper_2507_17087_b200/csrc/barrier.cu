@@ -94,6 +94,12 @@ extern "C" int pm_peer_copy_barrier(const pm_peer_barrier_view* v, const pm_peer
   if (!v || !v->epoch || !ticket || n < 0 || n > PM_PEER_COPY_MAX || (n > 0 && !copies) ||
       v->world < 1 || v->world > PM_BARRIER_MAX_RANKS || v->rank < 0 || v->rank >= v->world)
     return pm::set_error("pm_peer_copy_barrier: bad arguments"), PM_ERR_INVALID;
+  if (v->world > 1) {  // the same view checks as pm_peer_barrier
+    if (!v->my_flags) return pm::set_error("pm_peer_copy_barrier: bad view"), PM_ERR_INVALID;
+    for (int q = 0; q < v->world; ++q)
+      if (q != v->rank && !v->peer_slot[q])
+        return pm::set_error("pm_peer_copy_barrier: missing peer slot %d", q), PM_ERR_INVALID;
+  }
   pm::CopySet cs{};
   long long words = 0;
   for (int k = 0; k < n; ++k) {

@@ -25,6 +25,9 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "pm_common.h"
 
@@ -170,6 +173,8 @@ struct Params {
   int debug_nostore;  // experiments only (PM_GEMM_NOSTORE): skip the C stores
   int tma_store;      // epilogue through smem + TMA bulk store (map_c valid)
   int* tile_counter;  // dynamic tile scheduler ticket (zeroed before each launch)
+  int ticket_end;     // draws per launch (tiles + one terminal draw per pair): the
+                      // draw ticket_end - 1 is the last and zeroes the counter
   int k_split;        // 1-SM kernel: K slices per output tile (<= 1: none); > 1 adds
                       // every slice's partial product into C with vector red.add
 };
@@ -875,6 +880,7 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
   auto publish_tile = [&]() -> int {  // leader producer: draw and publish
     mbar_wait(&qempty[q_slot], q_phase ^ 1);
     const int t = atomicAdd(p.tile_counter, 1);
+    if (t == p.ticket_end - 1) atomicExch(p.tile_counter, 0);  // every pair has drawn
     tileq[q_slot] = t;
     const uint32_t peer_q = mapa_shared(smem_u32(&tileq[q_slot]), 1);
     asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(peer_q), "r"(t) : "memory");
@@ -1109,6 +1115,42 @@ extern "C" int pm_gemm_tf32(const float* A, int64_t lda, const float* Bt, int64_
   return PM_OK;
 }
 
+namespace pm::gemm {
+// Scheduler tickets (4-byte counters, one per 128-byte line): per (device,
+// stream) for eager launches, fresh for each captured launch.  Never freed --
+// library scratch that lives as long as the process, like the module state.
+static int tile_ticket(int dev, void* stream, int** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, void*>, int*> per_stream;
+  static int* pool[64] = {nullptr};
+  static int pool_used[64] = {0};
+  constexpr int kPool = 256;
+  std::lock_guard<std::mutex> lock(mu);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  PM_CUDA_TRY(cudaStreamIsCapturing((cudaStream_t)stream, &cs));
+  const bool captured = cs != cudaStreamCaptureStatusNone;
+  if (!captured) {
+    auto it = per_stream.find({dev, stream});
+    if (it != per_stream.end()) return *out = it->second, PM_OK;
+  }
+  if (!pool[dev] || pool_used[dev] == kPool) {
+    // a new block (cudaMalloc is legal during a capture only in relaxed mode;
+    // every launch zeroes its ticket with a stream-ordered memset, so the block
+    // needs no initialisation)
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    PM_CUDA_TRY(cudaThreadExchangeStreamCaptureMode(&mode));
+    cudaError_t e = cudaMalloc(&pool[dev], kPool * 128);
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    if (e != cudaSuccess)
+      return pm::set_error("tile ticket allocation: %s", cudaGetErrorString(e)), PM_ERR_CUDA;
+    pool_used[dev] = 0;
+  }
+  int* t = pool[dev] + 32 * pool_used[dev]++;
+  if (!captured) per_stream[{dev, stream}] = t;
+  return *out = t, PM_OK;
+}
+}  // namespace pm::gemm
+
 extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t ldb, void* C,
                             int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t c_bf16,
                             int32_t accumulate, void* stream) {
@@ -1156,6 +1198,8 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
   if (const char* g = getenv("PM_GEMM_GROUP")) p.group_m = atoi(g) > 0 ? atoi(g) : p.group_m;
   p.debug_nostore = getenv("PM_GEMM_NOSTORE") ? 1 : 0;
   static bool attr_done[64] = {false};
+  static std::mutex init_mu;
+  std::lock_guard<std::mutex> init_lock(init_mu);  // the per-device statics below
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return pm::set_error("pm_gemm_bf16: device id"), PM_ERR_UNSUPPORTED;
@@ -1220,12 +1264,15 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
         if (r != CUDA_SUCCESS)
           return pm::set_error("cuTensorMapEncodeTiled(C) failed: %d", (int)r), PM_ERR_CUDA;
       }
-      // tile-scheduler ticket: a ring of 64 counters per device (library
-      // scratch), zeroed on the launch stream
-      static int* counters[64] = {nullptr};
-      static unsigned next_slot[64] = {0};
-      if (!counters[dev]) PM_CUDA_TRY(cudaMalloc(&counters[dev], 64 * 128));
-      p.tile_counter = counters[dev] + (next_slot[dev]++ % 64) * 32;
+      // tile-scheduler ticket: one counter per (device, stream) -- launches on
+      // one stream are serialised, so they may share it -- and a dedicated one
+      // for every launch captured into a CUDA graph (a replay then never shares
+      // its ticket with an eager launch).  The kernel's last draw zeroes it
+      // again (self-resetting); the stream-ordered memset keeps a launch safe
+      // even after an aborted one.
+      rc = tile_ticket(dev, stream, &p.tile_counter);
+      if (rc) return rc;
+      p.ticket_end = (int)(pairs_needed + pairs);
       PM_CUDA_TRY(cudaMemsetAsync(p.tile_counter, 0, sizeof(int), (cudaStream_t)stream));
       wide::k_gemm_bf16_wide<<<(unsigned)(2 * pairs), wide::kThreadsW, wide::SMEMW,
                                (cudaStream_t)stream>>>(ma, mb, mc, p);

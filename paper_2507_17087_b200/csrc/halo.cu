@@ -439,6 +439,7 @@ k_halo2d_count(Strip2D h, int npairs, long long* __restrict__ tile_cnt,
   // the last warp to finish does the block's epilogue; the others leave at once (a
   // block-wide barrier here kept 7 warps waiting for the slowest one)
   __threadfence_block();
+  __syncwarp();  // every lane's shared atomics / s_any store precede lane 0's ticket
   int last = 0;
   if (lane == 0) last = atomicAdd(&s_done, 1) == kPartWarps - 1;
   if (!__shfl_sync(0xffffffffu, last, 0)) return;

@@ -315,6 +315,49 @@ struct Gen {
     return total > 0xFFFFFFFFull;
   }
 
+  // Diagnostic twin of pm_point for one failing point (pm_map_probe): on a
+  // failure it stores the whole register file (each register as two 64-bit
+  // words, sign-extended) so the host can format the reference's message with
+  // the operand values of the failing site, e.g. "index (3, 8) out of range
+  // for shape (2, 2)" (spaces.py:215-221, dsl/interp.py:207-214,245-258).
+  std::string emit_probe() {
+    const int k = p->n_coords;
+    std::ostringstream q;
+    o.str("");
+    o << "// generated by libmapple_b200 (K1 failure probe)\n" << kPrelude;
+    o << "#undef PM_FAIL\n#define PM_FAIL(s) do { *site_out = (s); goto pm_fail_; } while (0)\n";
+    o << "__device__ __noinline__ int pm_point_probe(";
+    for (int i = 0; i < k; ++i) o << "long long c" << i << ", ";
+    o << "int* __restrict__ site_out, long long* __restrict__ dump) {\n";
+    for (int r = 0; r < p->n_regs; ++r) o << "  " << kSigned[w(r)] << " r" << r << " = 0;\n";
+    body();
+    o << "  PM_FAIL(0xFFFF);\npm_fail_:\n";
+    for (int r = 0; r < p->n_regs; ++r)
+      o << "  dump[" << 2 * r << "] = (long long)r" << r << "; dump[" << 2 * r + 1
+        << "] = (long long)((__int128)r" << r << " >> 64);\n";
+    o << "  return -1;\n}\n\n";
+    o << "extern \"C\" __global__ void pm_map_probe(const int* pts, long long idx, "
+         "long long* dump, int* site) {\n  if (threadIdx.x | blockIdx.x) return;\n";
+    if (p->implicit) {
+      o << "  unsigned long long t = (unsigned long long)idx;\n";
+      for (int i = k - 1; i >= 0; --i) {
+        if (i == 0) o << "  long long c0 = (long long)t;\n";
+        else
+          o << "  long long c" << i << " = (long long)(t % " << p->extents[i] << "ULL); t /= "
+            << p->extents[i] << "ULL;\n";
+      }
+      o << "  (void)pts;\n";
+    } else {
+      for (int i = 0; i < k; ++i) o << "  long long c" << i << " = pts[idx * " << k << " + " << i << "];\n";
+    }
+    o << "  int s = -1;\n  const int r = pm_point_probe(";
+    for (int i = 0; i < k; ++i) o << "c" << i << ", ";
+    o << "&s, dump);\n  site[0] = r < 0 ? s : -1;\n  site[1] = r;\n}\n";
+    std::string out = o.str();
+    o.str("");
+    return out;
+  }
+
   std::string emit() {
     const int k = p->n_coords;
     const bool impl = p->implicit != 0;
@@ -591,7 +634,7 @@ int nvrtc_compile(const std::string& src, std::vector<char>* cubin, bool with_pa
   return PM_OK;
 }
 
-int generate(const pm_program* prog, std::string* out) {
+int generate(const pm_program* prog, std::string* out, std::string* probe = nullptr) {
   if (!prog || (prog->n_insns > 0 && !prog->insns) || (prog->n_regs > 0 && !prog->reg_width))
     return set_error("null program"), PM_ERR_INVALID;
   if (prog->implicit && prog->n_coords > 0 && !prog->extents)
@@ -600,6 +643,7 @@ int generate(const pm_program* prog, std::string* out) {
   g.p = prog;
   int rc = g.check();
   if (rc) return rc;
+  if (probe) *probe = g.emit_probe();
   *out = g.emit();
   return PM_OK;
 }
@@ -647,6 +691,14 @@ int pm_compile_check(const pm_program* prog) {
   return pm::nvrtc_compile(src, &cubin);
 }
 
+int pm_compile_check_probe(const pm_program* prog) {
+  std::string src, probe;
+  int rc = pm::generate(prog, &src, &probe);
+  if (rc) return rc;
+  std::vector<char> cubin;
+  return pm::nvrtc_compile(probe, &cubin);
+}
+
 int pm_compile_check_fused(const pm_program* prog) {
   std::string src;
   int rc = pm::generate(prog, &src);
@@ -658,8 +710,8 @@ int pm_compile_check_fused(const pm_program* prog) {
 int pm_plan_create(const pm_program* prog, pm_plan** out) {
   if (!out) return pm::set_error("null out"), PM_ERR_INVALID;
   *out = nullptr;
-  std::string src;
-  int rc = pm::generate(prog, &src);
+  std::string src, probe;
+  int rc = pm::generate(prog, &src, &probe);
   if (rc) return rc;
   std::vector<char> cubin;
   rc = pm::nvrtc_compile(src, &cubin);
@@ -684,7 +736,9 @@ int pm_plan_create(const pm_program* prog, pm_plan** out) {
   }
   p->n_coords = prog->n_coords;
   p->implicit = prog->implicit;
+  p->n_regs = prog->n_regs;
   p->src = src;
+  p->probe_src = probe;
   *out = p;
   return PM_OK;
 }
@@ -694,6 +748,7 @@ void pm_plan_destroy(pm_plan* plan) {
   const pm::Driver* d = pm::driver();
   if (d && plan->mod) d->moduleUnload(plan->mod);
   if (d && plan->fused_mod) d->moduleUnload(plan->fused_mod);
+  if (d && plan->probe_mod) d->moduleUnload(plan->probe_mod);
   delete plan;
 }
 
@@ -720,6 +775,32 @@ int pm_map_batch(const pm_plan* plan, const int32_t* points, int64_t n, int64_t 
                   (void*)&vec_ok};
   PM_CU_TRY(d->launchKernel(plan->fn, (unsigned)blocks, 1, 1, threads, 1, 1, 0,
                             (CUstream)stream, args, nullptr));
+  return PM_OK;
+}
+
+int pm_plan_regs(const pm_plan* plan) { return plan ? plan->n_regs : -1; }
+
+int pm_map_probe(pm_plan* plan, const int32_t* points, int64_t index, int64_t* dump,
+                 int32_t* site, void* stream) {
+  if (!plan || !dump || !site || index < 0 || (!plan->implicit && plan->n_coords > 0 && !points))
+    return pm::set_error("pm_map_probe: bad arguments"), PM_ERR_INVALID;
+  const pm::Driver* d = pm::driver();
+  if (!d) return PM_ERR_CUDA;
+  {
+    std::lock_guard<std::mutex> lk(plan->fused_mu);
+    if (!plan->probe_fn) {  // compiled on the first failure only
+      std::vector<char> cubin;
+      int rc = pm::nvrtc_compile(plan->probe_src, &cubin);
+      if (rc) return rc;
+      PM_CU_TRY(d->moduleLoadData(&plan->probe_mod, cubin.data()));
+      PM_CU_TRY(d->moduleGetFunction(&plan->probe_fn, plan->probe_mod, "pm_map_probe"));
+    }
+  }
+  const int32_t* pts = points;
+  long long idx = index;
+  void* args[] = {(void*)&pts, (void*)&idx, (void*)&dump, (void*)&site};
+  PM_CU_TRY(d->launchKernel(plan->probe_fn, 1, 1, 1, 32, 1, 1, 0, (CUstream)stream, args,
+                            nullptr));
   return PM_OK;
 }
 

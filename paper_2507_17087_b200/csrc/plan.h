@@ -12,7 +12,11 @@ struct pm_plan {
   int n_coords = 0;
   int implicit = 0;
   int device = 0;
+  int n_regs = 0;
   std::string src;          // generated K1 source (the fused module extends it)
+  std::string probe_src;    // failure probe (pm_map_probe), compiled on first use
+  CUmodule probe_mod = nullptr;
+  CUfunction probe_fn = nullptr;
   // fused map + partition kernels (K1 + K2 in two passes), built on first use
   std::mutex fused_mu;
   bool fused_ready = false;

@@ -233,6 +233,11 @@ def map_launch_sharded(fn, ispace, *, rank: int = 0, world: int = 1, group=None,
     torch = native.require_cuda()
     import torch.distributed as dist
 
+    if stream is not None and stream != torch.cuda.current_stream():
+        # the kernels and the collectives (which join the current stream) on one stream
+        with torch.cuda.stream(stream):
+            return map_launch_sharded(fn, ispace, rank=rank, world=world, group=group,
+                                      exchange=exchange, fused=fused, stream=None)
     ispace = tuple(int(e) for e in ispace)
     n = 1
     for e in ispace:

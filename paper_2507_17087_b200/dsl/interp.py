@@ -28,7 +28,7 @@ from collections import OrderedDict
 from ..errors import EvalError, LoweringError, NativeError, NoBinding
 from ..spaces import MachineShape
 from . import ast as A
-from .lower import INT32, Lowerer, ProcRef, lower_mapping, split_plan
+from .lower import INT32, Lowerer, ProcRef, format_site, lower_mapping, split_plan
 
 __all__ = ["Evaluator", "MappingFunction", "PointProgram", "ProcRef", "compile_mapper",
            "eval_mapping"]
@@ -74,6 +74,13 @@ class PointProgram:
 
         native.check(native.lib().pm_compile_check(ctypes.byref(self.c_program)),
                      "pm_compile_check")
+
+    def compile_check_probe(self) -> None:
+        """NVRTC-compile the failure probe of this program (no GPU)."""
+        from .. import native
+
+        native.check(native.lib().pm_compile_check_probe(ctypes.byref(self.c_program)),
+                     "pm_compile_check_probe")
 
     def compile_check_fused(self) -> None:
         """NVRTC-compile the fused map + partition kernels of this program (no GPU)."""
@@ -138,15 +145,50 @@ class PointProgram:
                 index_base, status.data_ptr(), scratch.data_ptr(), scratch.numel(),
                 native.stream_ptr(stream)), "pm_map_scatter")
 
-    def raise_for(self, status_word: int) -> None:
-        """Re-raise the failure a status word encodes (no-op for 'no failure')."""
+    def raise_for(self, status_word: int, points=None) -> None:
+        """Re-raise the failure a status word encodes (no-op for 'no failure'):
+        the reference's exception for the lowest failing point, with its exact
+        message -- a site whose message quotes per-point values (an index tuple,
+        a tuple index, a dimension) is formatted from that point's registers,
+        read back by the failure probe (pm_map_probe).  `points`: the explicit
+        int32 points of the failing launch (None in implicit mode)."""
         if status_word in (-1, (1 << 64) - 1):
             return
         status_word &= (1 << 64) - 1
         site = status_word & 0xFFFF
         if site >= len(self.sites):
             raise EvalError("mapping function evaluation failed")
-        raise copy.copy(self.sites[site])
+        exc = copy.copy(self.sites[site])
+        fmt = self.lowered.program.site_fmts.get(site)
+        if fmt is not None:
+            regs, got = self.probe(status_word >> 16, points)
+            if got != site:
+                raise NativeError(f"failure probe reached site {got}, the launch site {site}")
+            exc = type(exc)(format_site(fmt, regs))
+        raise exc
+
+    def probe(self, index: int, points=None):
+        """(registers, site) of point `index` evaluated by the failure probe."""
+        from .. import native
+
+        torch = native.require_cuda()
+        dev = points.device if points is not None else \
+            torch.device("cuda", torch.cuda.current_device())
+        with torch.cuda.device(dev):
+            plan = self.plan(dev.index)
+            nregs = native.lib().pm_plan_regs(plan)
+            dump = torch.zeros(2 * max(nregs, 1), dtype=torch.int64, device=dev)
+            site = torch.full((2,), -1, dtype=torch.int32, device=dev)
+            native.check(native.lib().pm_map_probe(
+                plan, 0 if points is None else points.data_ptr(), int(index), dump.data_ptr(),
+                site.data_ptr(), native.stream_ptr(None)), "pm_map_probe")
+            words = dump.cpu().tolist()
+            got = int(site[0].item())
+        regs = []
+        for r in range(nregs):
+            v = (words[2 * r] & ((1 << 64) - 1)) | (words[2 * r + 1] << 64)
+            regs.append(v)
+        return regs, got
 
     @staticmethod
     def failing_index(status_word: int) -> int | None:
@@ -203,7 +245,7 @@ def _run_points(pp: PointProgram, pts_list) -> list[tuple[int, int]]:
     status = torch.full((1,), -1, dtype=torch.int64, device=dev)
     pp.launch(pts, n, 0, out, status)
     word = int(status.item())
-    pp.raise_for(word)
+    pp.raise_for(word, pts)
     return out[:n].tolist()
 
 
@@ -263,11 +305,67 @@ class MappingFunction:
                                                    k, True)
         return pp
 
+    # launches up to this many points are mapped whole on the first single-point
+    # call and answered from the host copy of their ids afterwards
+    LOOKUP_MAX_POINTS = 1 << 22
+    LOOKUP_LAUNCHES = 8
+
     def __call__(self, ipoint, ispace) -> tuple[int, int]:
+        """One point -> (node, proc): the reference's per-point plugin call
+        (MappingFn, tasksim/sim.py:44), as driven point by point by cmd_map
+        (cli.py:158-161) and shard_policy (tasksim/sim.py:78).
+
+        The first call for a launch maps every point of it on the GPU (K1,
+        implicit row-major mode) and keeps the ids on the host, so the
+        reference's O(points x depth) call pattern costs one launch plus
+        lookups.  A point that failed in that launch, a point outside the
+        launch and launches above LOOKUP_MAX_POINTS take the single-point
+        device path, which raises the reference's exception for it."""
         ipoint, ispace = tuple(ipoint), tuple(ispace)
+        ids = self._launch_ids(ispace)
+        if ids is not None and len(ipoint) == len(ispace):
+            lin = 0
+            for c, e in zip(ipoint, ispace):
+                if not (type(c) is int and 0 <= c < e):
+                    break
+                lin = lin * e + c
+            else:
+                pid = ids[lin]
+                if pid >= 0:
+                    return divmod(pid, self.machine.procs_per_node)
         pp = self.program_for(ispace, implicit=False, k=len(ipoint))
         pid = _run_points(pp, [ipoint])[0]
         return divmod(pid, self.machine.procs_per_node)
+
+    def _launch_ids(self, ispace):
+        """Host copy (array of int32, -1 = failing point) of the whole launch's
+        processor ids, computed by K1; None for launches too large to keep."""
+        cache = self.__dict__.setdefault("_ids_cache", OrderedDict())
+        with self._lock:
+            hit = cache.get(ispace)
+            if hit is not None:
+                cache.move_to_end(ispace)
+                return hit
+        total = 1
+        for e in ispace:
+            if type(e) is not int or e <= 0:
+                return None
+            total *= e
+        if total > self.LOOKUP_MAX_POINTS:
+            return None
+        from array import array
+
+        try:
+            dev_ids = self.map_ispace(ispace, check=False)
+        except LoweringError:
+            return None  # the single-point path reports it
+        ids = array("i")
+        ids.frombytes(dev_ids.cpu().numpy().tobytes())
+        with self._lock:
+            cache[ispace] = ids
+            while len(cache) > self.LOOKUP_LAUNCHES:
+                cache.popitem(last=False)
+        return ids
 
     # -- batched device API -----------------------------------------------------
 
@@ -352,7 +450,7 @@ class MappingFunction:
         pp.map_scatter(points, count, pfirst, nprocs, out=ids, perm=perm, status=status,
                        scratch=scratch, stream=stream)
         if check:
-            pp.raise_for(int(status.item()))
+            pp.raise_for(int(status.item()), points)
         own = Ownership(counts, offsets, perm[:count])
         return (own, ids[:count]) if with_ids else own
 
@@ -374,7 +472,7 @@ class MappingFunction:
             pp = self.program_for(tuple(ispace), implicit=False, k=k)
             pp.launch(points, n, 0, out, status, stream)
             if check:
-                pp.raise_for(int(status.item()))
+                pp.raise_for(int(status.item()), points)
         return out[:n]
 
 

@@ -111,6 +111,23 @@ def _is_int(v) -> bool:
     return isinstance(v, (int, Reg)) and not isinstance(v, bool)
 
 
+def _tuple_pieces(vals) -> list:
+    """Message pieces printing a tuple of ints / registers as Python does."""
+    out = ["("]
+    for k, v in enumerate(vals):
+        if k:
+            out.append(", ")
+        out.append(v)
+    out.append(",)" if len(vals) == 1 else ")")
+    return out
+
+
+def format_site(fmt: tuple, regs) -> str:
+    """The message of a site from its pieces and the failing point's registers."""
+    return "".join(p if isinstance(p, str) else str(regs[p[1]]) if isinstance(p, tuple)
+                   else str(p) for p in fmt)
+
+
 def type_name(v) -> str:
     if isinstance(v, (bool, int, Reg)):
         return "Int"
@@ -161,6 +178,7 @@ class Program:
         self.const_insns: list[tuple] = []
         self.body: list = []                # insn tuples and ("if", cond, then, else)
         self.sites: list[Exception] = []
+        self.site_fmts: dict[int, tuple] = {}   # site -> message pieces (str / int / ("r", id))
         self._site_keys: dict = {}
         self.n_insns = 0
         self.coords: list[Reg] = []
@@ -169,12 +187,19 @@ class Program:
         self.regs.append([lo, hi])
         return Reg(len(self.regs) - 1, lo, hi)
 
-    def site(self, exc: Exception) -> int:
-        key = (type(exc), str(exc))
+    def site(self, exc: Exception, fmt: tuple | None = None) -> int:
+        """A failure site.  `fmt` (for messages that quote per-point values) is a
+        sequence of str pieces and Reg / int operands: the host formats the
+        reference's message from the registers of the failing point (probed on
+        the device, PointProgram.raise_for)."""
+        key = (type(exc), str(exc), None if fmt is None else tuple(
+            ("r", x.id) if isinstance(x, Reg) else x for x in fmt))
         sid = self._site_keys.get(key)
         if sid is None:
             sid = len(self.sites)
             self.sites.append(exc)
+            if fmt is not None:
+                self.site_fmts[sid] = key[2]
             self._site_keys[key] = sid
         return sid
 
@@ -255,10 +280,10 @@ class Lowerer:
 
     # -- emission helpers ----------------------------------------------------------
 
-    def fail(self, exc: Exception):
+    def fail(self, exc: Exception, fmt: tuple | None = None):
         if self.prog is None:
             raise exc
-        self._emit((OP_FAIL, -1, -1, -1, -1, self.prog.site(exc), 0, 0))
+        self._emit((OP_FAIL, -1, -1, -1, -1, self.prog.site(exc, fmt), 0, 0))
         raise _Dead()
 
     def _emit(self, insn):
@@ -665,7 +690,8 @@ class Lowerer:
                 self.fail(EvalError(f"index {i} out of range for tuple of rank {n}"))
             return tup[i]
         if i.lo < -n or i.hi >= n:
-            site = self.prog.site(EvalError(f"index out of range for tuple of rank {n}"))
+            site = self.prog.site(EvalError(f"index out of range for tuple of rank {n}"),
+                                  ("index ", i, f" out of range for tuple of rank {n}"))
             self._emit((OP_CHECK, -1, i.id, -1, -1, site, -n, n))
             i = Reg(i.id, max(i.lo, -n), min(i.hi, n - 1))
         cands = list(range(i.lo, i.hi + 1))
@@ -729,7 +755,8 @@ class Lowerer:
                     self.fail(EvalError(f"dimension {single} out of range for rank {r}"))
                 return space.shape[single]
             if single.lo < 0 or single.hi >= r:
-                site = self.prog.site(EvalError(f"dimension out of range for rank {r}"))
+                site = self.prog.site(EvalError(f"dimension out of range for rank {r}"),
+                                      ("dimension ", single, f" out of range for rank {r}"))
                 self._emit((OP_CHECK, -1, single.id, -1, -1, site, 0, r))
                 single = Reg(single.id, max(single.lo, 0), min(single.hi, r - 1))
             return self._select(single, [(j, space.shape[j])
@@ -747,17 +774,18 @@ class Lowerer:
             except ProcMapError as exc:
                 self.fail(EvalError(str(exc)))
             return ProcRef(node, proc)
+        # the reference's message quotes the whole index tuple (spaces.py:215-221)
+        msg = ["index ", *_tuple_pieces(coords), f" out of range for shape {space.shape}"]
         for c, s in zip(coords, space.shape):
             if isinstance(c, int) and not 0 <= c < s:
-                self.fail(EvalError(
-                    f"index {tuple(coords)} out of range for shape {space.shape}"))
+                self.fail(EvalError(f"index out of range for shape {space.shape}"), tuple(msg))
         site = None
         cur = []
         for c, s in zip(coords, space.shape):
             if isinstance(c, Reg) and (c.lo < 0 or c.hi >= s):
                 if site is None:
                     site = self.prog.site(EvalError(
-                        f"index out of range for shape {space.shape}"))
+                        f"index out of range for shape {space.shape}"), tuple(msg))
                 self._emit((OP_CHECK, -1, c.id, -1, -1, site, 0, s))
                 c = Reg(c.id, max(c.lo, 0), min(c.hi, s - 1))
             cur.append(c)

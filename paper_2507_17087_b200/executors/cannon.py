@@ -96,7 +96,8 @@ def cannon_schedule(q: int, c: int, coord):
 
 class MappedCannon:
     def __init__(self, N: int, *, layers: int = 1, rank: int = 0, world: int = 1, group=None,
-                 dtype: str = "fp32", machine=None, seed: int = 0, graph: bool = False):
+                 dtype: str = "fp32", machine=None, seed: int = 0, graph: bool = False,
+                 program: str | None = None, task: str | None = None):
         torch = native.require_cuda()
         self.graph = graph
         self._graphs = {}
@@ -118,13 +119,15 @@ class MappedCannon:
         # Mapple mapping of the tile launch (K1)
         if machine is None:
             machine = (2, world // 2) if (c == 1 and world % 2 == 0 and world > 2) else (world, 1)
-        prog = parse(HIER_MAPPERS)
+        # any Mapple program with a tile-launch task may place the tiles, e.g. the
+        # reference corpus' `cannon_mm` (matmul_mappers.mapper); default: HIER_MAPPERS
+        prog = parse(program if program is not None else HIER_MAPPERS)
         if c == 1:
-            fn = compile_mapper(prog, "cannon", MachineShape("GPU", *machine))
+            fn = compile_mapper(prog, task or "cannon", MachineShape("GPU", *machine))
             owners = fn.map_ispace((q, q)).tolist()
             coords = [(i, j, 0) for i in range(q) for j in range(q)]
         else:
-            fn = compile_mapper(prog, "solomonik", MachineShape("GPU", *machine))
+            fn = compile_mapper(prog, task or "solomonik", MachineShape("GPU", *machine))
             owners = fn.map_ispace((q, q, c)).tolist()
             coords = [(i, j, l) for i in range(q) for j in range(q) for l in range(c)]
         if sorted(owners) != list(range(world)):
@@ -157,7 +160,12 @@ class MappedCannon:
         self._bar = PeerBarrier(rank, world, group) if world > 1 else None
         # small blocks: the SMs copy a round's blocks and run its barrier in one launch
         # (latency-bound rounds, configs[0]); large ones go to the copy engines
-        self._fused_pulls = nb * nb * (4 if dtype == "fp32" else 2) <= (8 << 20)
+        # (pm_peer_copy_barrier copies 16-byte words: checked once here, so a step can
+        # never fail half-way through its schedule and leave the peers in a barrier)
+        blk = nb * nb * (4 if dtype == "fp32" else 2)
+        ptrs = [p for v in self.peers.ptrs.values() for p in v]
+        self._fused_pulls = (blk <= (8 << 20) and blk % 16 == 0 and (nb * (4 if dtype == "fp32"
+                             else 2)) % 16 == 0 and all(p % 16 == 0 for p in ptrs))
         self._dist = dist if world > 1 else None
         self.step_i = 0
         self.moved_blocks = 0
@@ -208,7 +216,8 @@ class MappedCannon:
             # the layers' adds into C[buf] date from two steps ago and all finished before
             # the previous step's barriers; the schedule's first barrier orders this zeroing
             # before any peer adds into it again
-            self.C[buf].zero_()
+            with torch.cuda.stream(cs):
+                self.C[buf].zero_()
         moved = 0
         first = True  # the first local product overwrites C (Cannon); 2.5D always adds
         pending = []  # a round's pulls, issued with its closing barrier (one launch)

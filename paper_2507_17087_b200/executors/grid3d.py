@@ -149,9 +149,9 @@ class MappedGemm3D:
         if self._dist:
             dist.barrier(group=group)
 
-    def _barrier(self):
+    def _barrier(self, stream=None):
         if self._bar is not None:  # stream-ordered: runs after the queued GEMMs
-            self._bar()
+            self._bar(stream)
 
     def step(self, stream=None):
         torch = native.require_cuda()
@@ -165,8 +165,9 @@ class MappedGemm3D:
             # before it joined the previous step's barrier, which we passed: zero it now,
             # and only then (barrier) may the peers add into it.  C[1-buf] -- the previous
             # step's result -- stays intact during this step.
-            self.C[buf].zero_()
-            self._barrier()
+            with torch.cuda.stream(cs):  # ordered with the GEMMs on cs
+                self.C[buf].zero_()
+            self._barrier(cs)
         for s in self.streams:
             s.wait_event(self.done)
         for name, q, (r0, r1), si, ev in self.pulls:

@@ -291,6 +291,9 @@ class MappedGemm:
         ka, kb = self.layout.a_slice[rank], self.layout.b_slice[rank]
         self.A[:, ka[0]:ka[1]] = synth(self.rows, ka, K, seed, self.device)
         self.Bt[:, kb[0]:kb[1]] = synth(self.cols, kb, K, seed + 1, self.device)
+        # the own slices are complete before any peer can learn their address (the
+        # handle exchange is collective): a peer's first pull never reads them early
+        torch.cuda.synchronize(self.device)
         self.peers = PeerBuffers({"A": self.A, "Bt": self.Bt}, rank, world, group)
         self._plan(block, a_chunks, copy_streams)
         self.done = torch.cuda.Event()

@@ -8,7 +8,8 @@ import sys
 from math import isqrt
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
 
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
@@ -74,6 +75,39 @@ def main():
                         "owners_ok": got == want})
             if world > 1:
                 dist.barrier()
+            ex.close()
+    if world == 4:
+        # BASELINE configs[0] exactly as the reference states it: the corpus' own
+        # `cannon_mm` (matmul_mappers.mapper, hierarchical_block2D) on
+        # MachineShape(GPU, 2, 2), fp32 N=1024; owners == the reference's
+        # assignment table (tests/golden/mappings.json, produced by running the
+        # reference), 12 block moves, full C vs float64
+        gold = json.loads((ROOT / "tests" / "golden" / "mappings.json").read_text())
+        case = next(c for c in gold["cases"] if c["name"] == "matmul_mappers:cannon_mm"
+                    and c["machine"] == [2, 2] and c["ispace"] == [2, 2])
+        ref_ids = [n * 2 + p for n, p in case["table"]]
+        for graph in (False, True):
+            ex = MappedCannon(1024, layers=1, rank=rank, world=world, dtype="fp32", seed=21,
+                              graph=graph, machine=(2, 2), program=gold["sources"][case["src"]],
+                              task="cannon_mm")
+            for _ in range(5):
+                ex.step()
+            C = ex.result()
+            torch.cuda.synchronize()
+            i, j, _ = ex.coord
+            nb = ex.nb
+            A = synth((i * nb, (i + 1) * nb), (0, 1024), 1024, 21, "cuda").double()
+            Bt = synth((j * nb, (j + 1) * nb), (0, 1024), 1024, 22, "cuda").double()
+            R = A @ Bt.T
+            err = float((C.double() - R).abs().max() / R.abs().max())
+            moves = [None] * world
+            dist.all_gather_object(moves, ex.moved_blocks)
+            got = [ex.owner[(a, b, 0)] for a in range(2) for b in range(2)]
+            out.append({"c": 1, "dtype": "fp32", "N": 1024, "graph": graph, "rank": rank,
+                        "err": err, "moves": sum(moves), "want_moves": 12,
+                        "owners_ok": got == ref_ids, "configs0_reference_owners": ref_ids,
+                        "owners": got})
+            dist.barrier()
             ex.close()
     allr = [out]
     if world > 1:

@@ -12,9 +12,19 @@ from paper_2507_17087_b200.dsl import lower as L
 
 
 class Fail(Exception):
-    def __init__(self, site):
+    def __init__(self, site, regs=None):
         super().__init__(site)
         self.site = site
+        self.regs = list(regs or [])
+
+
+def message(lowered, fail: "Fail") -> str:
+    """The exception message the product formats for a failure (the registers a
+    site's message quotes come from pm_map_probe on the GPU; here from the run)."""
+    fmt = lowered.program.site_fmts.get(fail.site)
+    if fmt is None:
+        return str(lowered.program.sites[fail.site])
+    return L.format_site(fmt, fail.regs)
 
 
 def run(lowered, point):
@@ -57,7 +67,7 @@ def run(lowered, point):
             x, y = regs[a], regs[b]
             if y == 0:
                 assert site >= 0, "unchecked division by zero"
-                raise Fail(site)
+                raise Fail(site, regs)
             if c & 1:
                 assert x >= 0 and y > 0
             put(d, x // y if op == L.OP_DIV else x % y)
@@ -70,9 +80,9 @@ def run(lowered, point):
             put(d, regs[a])
         elif op == L.OP_CHECK:
             if not lo <= regs[a] < hi:
-                raise Fail(site)
+                raise Fail(site, regs)
         elif op == L.OP_FAIL:
-            raise Fail(site)
+            raise Fail(site, regs)
         elif op == L.OP_IF:
             els, end = match[pc]
             if regs[a] == 0:

@@ -23,15 +23,17 @@ def _points(ispace):
 
 
 def _expect(table, ppn):
-    ids, errs = [], []
+    ids, errs, msgs = [], [], []
     for row in table:
         if isinstance(row, dict):
             ids.append(-1)
             errs.append(row["error"])
+            msgs.append(row["message"])
         else:
             ids.append(row[0] * ppn + row[1])
             errs.append(None)
-    return ids, errs
+            msgs.append(None)
+    return ids, errs, msgs
 
 
 @pytest.fixture(scope="module")
@@ -53,9 +55,10 @@ def test_golden_tables_implicit_and_explicit(built, cuda):
     for case, fn, pp in built:
         ispace = tuple(case["ispace"])
         ppn = case["machine"][1]
-        want, errs = _expect(case["table"], ppn)
+        want, errs, msgs = _expect(case["table"], ppn)
         n = len(want)
         status = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        pts = None
         if pp.lowered.implicit:
             got = fn.map_ispace(ispace, check=False, status=status)
         else:
@@ -67,8 +70,10 @@ def test_golden_tables_implicit_and_explicit(built, cuda):
         assert pp.failing_index(word) == first_bad
         if first_bad is not None:
             with pytest.raises(Exception) as info:
-                pp.raise_for(word)
+                pp.raise_for(word, pts)
+            # the reference's class and exact message (point values from the probe)
             assert type(info.value).__name__ == errs[first_bad]
+            assert str(info.value) == msgs[first_bad], (case["name"], first_bad)
 
 
 def test_single_point_api_and_eval_mapping(cuda):
@@ -85,6 +90,7 @@ def test_single_point_api_and_eval_mapping(cuda):
                 with pytest.raises(Exception) as info:
                     fn(pts[i], ispace)
                 assert type(info.value).__name__ == want["error"]
+                assert str(info.value) == want["message"]
             else:
                 assert list(fn(pts[i], ispace)) == want
             if "eval_table" in c:
@@ -93,6 +99,7 @@ def test_single_point_api_and_eval_mapping(cuda):
                     with pytest.raises(Exception) as info:
                         eval_mapping(prog, c["func"], pts[i], ispace, machine)
                     assert type(info.value).__name__ == want["error"]
+                    assert str(info.value) == want["message"]
                 else:
                     assert list(eval_mapping(prog, c["func"], pts[i], ispace, machine)) == want
 

@@ -34,6 +34,8 @@ def _compare(lowered, ispace, table, ppn):
         except irsim.Fail as f:
             assert isinstance(want, dict), (pt, "kernel failed", lowered.program.sites[f.site], want)
             assert type(lowered.program.sites[f.site]).__name__ == want["error"], pt
+            # the reference's exact message, point-specific values included
+            assert irsim.message(lowered, f) == want["message"], (pt, want)
             continue
         assert not isinstance(want, dict), (pt, got, want)
         assert list(divmod(got, ppn)) == want, pt

@@ -57,6 +57,26 @@ def test_codegen_compiles_with_nvrtc(case):
         assert "pm_map_points" in src
         pp.compile_check()
         pp.compile_check_fused()
+        pp.compile_check_probe()
+
+
+def test_failure_probes_compile_for_message_sites():
+    """Every golden program whose failures quote per-point values has a probe
+    that NVRTC accepts (the GPU run formats the messages from it)."""
+    done = 0
+    for case in mapping_cases():
+        if not isinstance(case["table"], list) or not any(
+                isinstance(r, dict) and "index" in r["message"] for r in case["table"]):
+            continue
+        fn = compile_mapper(parse(case["source"]), case["task"],
+                            MachineShape("GPU", *case["machine"]))
+        pp = fn.program_for(case["ispace"], implicit=True)
+        if pp.lowered.program.site_fmts:
+            pp.compile_check_probe()
+            done += 1
+        if done >= 6:
+            break
+    assert done >= 1
 
 
 def test_bad_program_is_rejected():
