@@ -11,9 +11,10 @@ tcgen05 GEMMs.  Time = CUDA events on the compute stream, max over ranks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-`--impl reference` times the reference-side CPU path (the oracle port: numpy
-float64 GEMM on a bounded sample of the same product, all host threads) on
-rank 0 and prints the same JSON line with "impl": "reference".
+`--impl reference` times the reference's CPU path on the host cores (rank 0):
+the unmodified reference (baseline/_ref) maps the launch with the same Mapple
+program, numpy float32 multiplies a bounded sample of the same product (the
+reference has no GEMM), and prints the same JSON line with "impl": "reference".
 """
 
 from __future__ import annotations
@@ -579,7 +580,7 @@ def run_e2e_pipelined_multi(args, ex, rank, world):
                          "separate streams, stream-ordered NCCL flags between GPUs"}
 
 
-def cpu_sample(args, threads=None):
+def cpu_sample(args, threads=None, seconds=None):
     """The oracle port on the host: numpy float64 C[0:r, 0:c] of the same product."""
     import numpy as np
     import torch
@@ -597,7 +598,7 @@ def cpu_sample(args, threads=None):
     t = time.perf_counter()
     C = sample_rows_cols(A, Bt)
     reps = 1
-    while time.perf_counter() - t < args.cpu_seconds:
+    while time.perf_counter() - t < (args.cpu_seconds if seconds is None else seconds):
         sample_rows_cols(A, Bt)
         reps += 1
     dt = (time.perf_counter() - t) / reps
@@ -702,14 +703,21 @@ def hot_path_kernels(args):
     if not args.no_cpu:
         # the reference's CPU path for this launch (oracle port of cmd_map's per-point
         # loop) on 1 core and on every core, bounded samples, extrapolated
-        from oracle.cpu_mapping_bench import cpu_mapping_rate
+        from oracle.cpu_mapping_bench import cpu_mapping_rate, reference_available
 
-        k1_cpu = cpu_mapping_rate(src, "t", ("GPU", 1, 8), (L, L), seconds=3.0)
-        k1_cpu.update({"kind": "port", "unit": "points/s",
+        kind = "reference" if reference_available() else "port"
+        k1_cpu = cpu_mapping_rate(src, "t", ("GPU", 1, 8), (L, L), seconds=3.0, kind=kind)
+        k1_cpu.update({"unit": "points/s",
                        "sample": "contiguous row-major slices of the 32768^2 launch, 3 s per "
-                                 "worker (full-launch time extrapolated)",
+                                 "worker (full-launch time extrapolated); kind reference = the "
+                                 "unmodified reference in baseline/_ref (compile_mapper + "
+                                 "per-point fn, cmd_map's loop)",
                        "k1_speedup_vs_all_cores": (n / (k1_ms * 1e-3)) /
                                                   k1_cpu["points_per_s_all"]})
+        if kind == "reference":  # the oracle port beside it
+            port = cpu_mapping_rate(src, "t", ("GPU", 1, 8), (L, L), seconds=2.0, kind="port")
+            k1_cpu["port"] = {k: port[k] for k in ("points_per_s_1core", "points_per_s_all",
+                                                   "cores")}
     # K2 reads the ids twice and writes the permutation; the scatter skips the read for
     # tiles whose 4096 ids are all equal (uniform): 8 + 4 * (non-uniform fraction) B/pt
     t = out.view(-1, 4096)
@@ -841,12 +849,15 @@ def main_ours(args):
         extra["pennant_hydro"] = guarded("pennant_hydro", hydro)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        C64, dt, fl, used = cpu_sample(args)
-        cpu = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": used,
-               "kind": "port",
-               "sample": f"numpy float64 C[0:{args.cpu_rows}, 0:{args.cpu_cols}] of the "
-                         f"{args.size}^3 product (full K), {dt:.2f} s each, repeated for "
-                         f"~{args.cpu_seconds:.0f} s"}
+        # the reference's CPU path of this workload (same as the --impl reference arm)
+        h = host_reference_step(args, world, args.cpu_seconds)
+        cpu = {"value": h["tflops"], "unit": "TFLOP/s", "cores": h["cores"],
+               "kind": h["mapping_kind"],
+               "sample": f"the reference (baseline/_ref) maps all {h['mapping_points']} C-block "
+                         f"points (every core), then {h['gemm_sample']} extrapolated to the "
+                         "full product (the reference has no GEMM, SURVEY F9)",
+               "parts": h}
+        C64, dt, fl, used = cpu_sample(args, seconds=0.0)
         # parity on the same sample: the GPU's C block starts at row/col 0 here
         from paper_2507_17087_b200.executors.summa import MappedGemm
 
@@ -944,44 +955,78 @@ def blas_threads():
     return lim, used
 
 
+def host_reference_step(args, world: int, seconds: float):
+    """One step of the reference's CPU path for the headline workload, on the host
+    cores: (1) the reference itself (baseline/_ref, unmodified) maps the SUMMA C-block
+    launch -- compile_mapper + the per-point loop of cmd_map (cli.py:149-161,
+    dsl/interp.py:401-433) over all (S/128)^2 points of the same Mapple program and
+    machine (G, 1) our arm uses, on every host core (contiguous slices, one worker
+    per core); (2) the block products, which the reference does not implement
+    (SURVEY F9), as numpy float32 GEMMs on every core -- a bounded sample
+    C[0:r, 0:c] with the full K, repeated for ~`seconds`, extrapolated to the whole
+    product.  Returns the step time and its parts."""
+    import numpy as np
+
+    from oracle.cpu_mapping_bench import cpu_mapping_rate, reference_available
+    from paper_2507_17087_b200.executors.summa import TILE_MAPPERS
+    from paper_2507_17087_b200.factorize import greedy_grid
+
+    S = args.size
+    nb = -(-S // 128)
+    src = TILE_MAPPERS.format(g0=greedy_grid(world, 2)[0])
+    kind = "reference" if reference_available() else "port"
+    m = cpu_mapping_rate(src, "gemm_decompose", ("GPU", world, 1), (nb, nb),
+                         seconds=min(3.0, seconds / 4), kind=kind)
+    t_map = nb * nb / m["points_per_s_all"]
+    lim, cores = blas_threads()
+    r, c = args.cpu_rows, args.cpu_cols
+    rng = np.random.default_rng(1234)
+    A = rng.uniform(-1, 1, (r, S)).astype(np.float32)
+    Bt = rng.uniform(-1, 1, (c, S)).astype(np.float32)
+    A[:64] @ Bt[:64].T  # BLAS warm-up
+    t = time.perf_counter()
+    reps = 0
+    while reps == 0 or time.perf_counter() - t < seconds:
+        A @ Bt.T
+        reps += 1
+    t_sample = (time.perf_counter() - t) / reps
+    t_gemm = t_sample * (S / r) * (S / c)
+    return {"ms_per_step": (t_map + t_gemm) * 1e3, "tflops": 2.0 * S ** 3 / (t_map + t_gemm) / 1e12,
+            "cores": max(cores, m["cores"]), "mapping_kind": kind,
+            "mapping_points": nb * nb, "mapping_points_per_s_all_cores": m["points_per_s_all"],
+            "mapping_points_per_s_1core": m["points_per_s_1core"], "mapping_s": t_map,
+            "gemm_sample": f"numpy float32 C[0:{r}, 0:{c}] (full K = {S}), {t_sample:.3f} s",
+            "gemm_sample_tflops": 2.0 * r * c * S / t_sample / 1e12, "gemm_s_extrapolated": t_gemm}
+
+
 def main_reference(args):
-    """Reference arm: the CPU path (oracle port) on the host cores, rank 0 only."""
+    """Reference arm: the reference's CPU path on the host cores, rank 0 only
+    (host_reference_step: the reference maps the launch, numpy multiplies)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import numpy as np
-
-    from oracle.numerics import sample_rows_cols
-
-    lim, cores = blas_threads()
-    S = args.size
-    r, c = args.cpu_rows, args.cpu_cols
-    rng = np.random.default_rng(1234)
-    A = rng.uniform(-1, 1, (r, S))
-    Bt = rng.uniform(-1, 1, (c, S))
-    for _ in range(max(0, min(args.warmup, 1))):
-        sample_rows_cols(A[:64], Bt[:64])
-    times = []
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     nsteps = max(1, min(args.steps, 3))
-    for _ in range(nsteps):  # each step: the bounded sample, repeated for ~cpu_seconds/nsteps
-        t = time.perf_counter()
-        reps = 0
-        while reps == 0 or time.perf_counter() - t < args.cpu_seconds / nsteps:
-            sample_rows_cols(A, Bt)
-            reps += 1
-        times.append((time.perf_counter() - t) / reps)
-    dt = statistics.mean(times)
-    v = 2.0 * r * c * S / dt / 1e12
-    lim.unregister() if hasattr(lim, "unregister") else None
+    steps = [host_reference_step(args, world, args.cpu_seconds / nsteps) for _ in range(nsteps)]
+    ms = statistics.mean(s["ms_per_step"] for s in steps)
+    v = 2.0 * args.size ** 3 / (ms * 1e-3) / 1e12
+    last = steps[-1]
+    S = args.size
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s",
-        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": len(times),
-        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "M": S, "N": S, "K": S, "mapping": "decompose"},
-        "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"numpy float64 C[0:{r}, 0:{c}] of the {S}^3 product "
-                                   "(full K) per step; the reference has no GEMM (SURVEY F9)"},
+        "n_gpus": world, "steps": nsteps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "M": S, "N": S, "K": S, "mapping": "decompose",
+                   "machine": [world, 1]},
+        "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": last["cores"],
+                         "kind": last["mapping_kind"],
+                         "sample": f"per step: the reference (baseline/_ref) maps all "
+                                   f"{last['mapping_points']} C-block points of the launch "
+                                   f"(compile_mapper + cmd_map's per-point loop, every core), "
+                                   f"then {last['gemm_sample']} extrapolated to the full product "
+                                   "(the reference has no GEMM, SURVEY F9)",
+                         "parts": last},
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
