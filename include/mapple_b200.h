@@ -183,18 +183,31 @@ int pm_halo_lists(const int32_t* owner, const int64_t* ext, int32_t rank,
  * sparse, so no per-(pair, tile) histogram is built):
  *   pm_halo_count    pair_counts[nprocs^2] and, in tile_scratch
  *                    (pm_halo_tile_scratch_bytes), each 8192-slot tile's output
- *                    offset;
+ *                    offset (and, after the scan, the total entry count);
  *   pm_halo_compact  every entry as (pair key, slot index = cell * 2R + 2n + (s>0))
- *                    in slot order into keys / slots [sum of pair_counts];
+ *                    in slot order into keys / slots [cap] (entries past cap dropped);
  *   (pm_partition of keys into nprocs^2 bins -> perm, counts, offsets)
  *   pm_halo_gather   cells[j] / dims[j] of slots[perm[j]] (dims nullable). */
 size_t pm_halo_tile_scratch_bytes(const int64_t* ext, int32_t rank);
 int pm_halo_count(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
                   int32_t nprocs, int64_t* pair_counts, void* tile_scratch, size_t bytes,
-                  void* stream);
+                  int64_t* total /* nullable: device copy of the entry count */, void* stream);
 int pm_halo_compact(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
-                    int32_t nprocs, void* tile_scratch, int32_t* keys, int64_t* slots,
+                    int32_t nprocs, void* tile_scratch, int32_t* keys, int64_t* slots, int64_t cap,
                     void* stream);
+/* Grouping without a permutation array: the stable partition of the compacted
+ * keys (only the first *total of the cap items; total = the device-side entry
+ * count, e.g. the sum of pair_counts) writes each entry's cells[] / dims[]
+ * at its grouped position, and pair_counts / pair_offsets.  No host
+ * synchronisation is needed between count, compaction and grouping when the
+ * caller sizes keys / slots / cells / dims with a capacity `cap` (entries
+ * past it are dropped; compare the returned total with cap).
+ * scratch: pm_halo_group_scratch_bytes(cap, nprocs). */
+size_t pm_halo_group_scratch_bytes(int64_t cap, int32_t nprocs);
+int pm_halo_group(const int32_t* keys, const int64_t* slots, int64_t cap, const int64_t* total,
+                  int32_t rank, int32_t nprocs, int64_t* pair_counts, int64_t* pair_offsets,
+                  int64_t* cells, int8_t* dims, void* scratch, size_t scratch_bytes,
+                  void* stream);
 int pm_halo_gather(const int32_t* perm, const int64_t* slots, int64_t n, int32_t rank,
                    int64_t* cells, int8_t* dims, void* stream);
 

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "pm_common.h"
 #include "stable_partition.cuh"
@@ -231,7 +232,7 @@ k_halo_count(Key key, long long n, int npairs, long long* __restrict__ tile_cnt,
 template <class Key>
 __global__ void __launch_bounds__(kPartThreads)
 k_halo_compact(Key key, long long n, long long ntiles, const long long* __restrict__ tile_off,
-               const long long* __restrict__ total, int* __restrict__ out_key,
+               const long long* __restrict__ total, long long cap, int* __restrict__ out_key,
                long long* __restrict__ out_slot) {
   const long long t = blockIdx.x;
   const long long lo = tile_off[t], hi = t + 1 < ntiles ? tile_off[t + 1] : *total;
@@ -264,8 +265,10 @@ k_halo_compact(Key key, long long n, long long ntiles, const long long* __restri
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (k[q] >= 0) {
-        out_key[pos] = k[q];
-        out_slot[pos] = i0 + q;
+        if (pos < cap) {
+          out_key[pos] = k[q];
+          out_slot[pos] = i0 + q;
+        }
         ++pos;
       }
     running += all;
@@ -303,6 +306,8 @@ constexpr int kStripRows = 64;                 // rows per block (one mask bit e
 #define PM_STRIP_MINB 4
 #endif
 constexpr int kStripBatch = PM_STRIP_BATCH;    // rows of loads in flight per thread
+static_assert(kStripRows % kStripBatch == 0, "the unclamped walk takes whole batches");
+
 
 struct Strip2D {
   const int* __restrict__ owner;
@@ -405,10 +410,13 @@ __device__ __forceinline__ void strip_rows(const Strip2D& h, long long r0, int n
     strip_walk<true>(h, r0, nr, c0, f);
 }
 
+inline size_t pad256(size_t b) { return (b + 255) / 256 * 256; }
+
 __global__ void __launch_bounds__(kPartThreads, PM_STRIP_MINB)
 k_halo2d_count(Strip2D h, int npairs, long long* __restrict__ tile_cnt,
                unsigned long long* __restrict__ pair_cnt, unsigned long long* __restrict__ warp_rows,
-               unsigned short* __restrict__ warp_pre) {
+               unsigned short* __restrict__ warp_pre, unsigned* __restrict__ wl_count,
+               unsigned* __restrict__ wl, unsigned* __restrict__ lane_mask) {
   extern __shared__ int sp[];  // [npairs]
   __shared__ int s_row[kStripRows][kPartWarps];
   __shared__ unsigned s_mask[kStripRows / 32][kPartWarps];
@@ -421,21 +429,31 @@ k_halo2d_count(Strip2D h, int npairs, long long* __restrict__ tile_cnt,
   const int nr = (int)min((long long)kStripRows, h.rows - r0);
   const long long c0 = (long long)seg * kStripCells + 4 * threadIdx.x;
   const bool active = c0 < h.cols;
-  bool any = false;
+  unsigned groups = 0;  // bit g: this thread's cells hold entries in rows 8g .. 8g + 7
   strip_rows(h, r0, nr, c0, [&](int i, const int4& up, const int4& cur, const int4& dn, int lf,
                                 int rt) {
     int k[16];
     const int n = active ? h.keys(up, cur, dn, lf, rt, k) : 0;
     if (n) {
-      any = true;
+      groups |= 1u << (i >> 3);
 #pragma unroll
-      for (int s = 0; s < 16; ++s)
-        if (k[s] >= 0) atomicAdd(&sp[k[s]], 1);
+      for (int q = 0; q < 16; ++q)
+        if (k[q] >= 0) atomicAdd(&sp[k[q]], 1);
     }
     const int tot = __reduce_add_sync(0xffffffffu, n);
     if (lane == 0) s_row[i][warp] = tot;
   });
-  if (any) s_any = 1;
+  if (groups) s_any = 1;
+  // per 8-row group, the lanes of this warp holding entries: the compaction loads only
+  // theirs (written only for warps with entries -- the only ones it reads)
+  if (__any_sync(0xffffffffu, groups != 0)) {
+    unsigned* lm = lane_mask + (((long long)blockIdx.y * h.nseg + seg) * kPartWarps + warp) * 8;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const unsigned m = __ballot_sync(0xffffffffu, groups >> g & 1);
+      if (lane == g) lm[g] = m;
+    }
+  }
   // the last warp to finish does the block's epilogue; the others leave at once (a
   // block-wide barrier here kept 7 warps waiting for the slowest one)
   __threadfence_block();
@@ -444,8 +462,8 @@ k_halo2d_count(Strip2D h, int npairs, long long* __restrict__ tile_cnt,
   if (lane == 0) last = atomicAdd(&s_done, 1) == kPartWarps - 1;
   if (!__shfl_sync(0xffffffffu, last, 0)) return;
   __threadfence_block();
-  // per tile (row): its entry count; per warp: which rows hold its entries (the
-  // compaction skips the rest) and, in non-empty tiles, its first entry within the tile
+  // per tile (row): its entry count; per warp: which rows hold its entries and, in
+  // non-empty tiles, its first entry within the tile
   const long long blk = (long long)blockIdx.y * h.nseg + seg;
 #pragma unroll
   for (int q = 0; q < kStripRows / 32; ++q) {
@@ -481,59 +499,190 @@ k_halo2d_count(Strip2D h, int npairs, long long* __restrict__ tile_cnt,
     for (int q = 0; q < kStripRows / 32; ++q)
       rows_hit |= (unsigned long long)s_mask[q][lane] << (32 * q);
     warp_rows[blk * kPartWarps + lane] = rows_hit;
+    // the compaction's work list: the units holding entries
+    if (rows_hit) wl[atomicAdd(wl_count, 1u)] = (unsigned)(blk * kPartWarps + lane);
   }
   if (s_any)
     for (int b = lane; b < npairs; b += 32)
       if (sp[b]) atomicAdd(pair_cnt + b, (unsigned long long)sp[b]);
 }
 
-__global__ void __launch_bounds__(32)
+// Persistent compaction over the count pass's work list (one item per (row block,
+// strip, warp) unit holding entries).  The unit's entries sit, per 8-row group, in the
+// cells of the lanes of that group's lane mask, in the rows of its row mask: one
+// (row, lane) combination per thread, row-major, so a vertical cut (one lane, every
+// row) fills a warp with 32 rows at once and a horizontal cut (every lane, one row)
+// with 32 lanes.  Each thread loads its four cells and their neighbours and computes
+// their entries; a segmented warp scan over the threads of one row (plus the part of
+// that row placed by the previous iteration) gives each entry its slot-order position.
+// Entries past `cap` are dropped.
+__global__ void __launch_bounds__(256)
 k_halo2d_compact(Strip2D h, const long long* __restrict__ tile_off,
                  const unsigned long long* __restrict__ warp_rows,
-                 const unsigned short* __restrict__ warp_pre, int* __restrict__ out_key,
-                 long long* __restrict__ out_slot) {
-  // one warp per CTA (x = strip * 8 + warp of the count pass): only the few warps holding
-  // entries stay resident, instead of 256-thread CTAs pinned by their one busy warp
-  const int seg = blockIdx.x / kPartWarps, warp = blockIdx.x % kPartWarps;
+                 const unsigned short* __restrict__ warp_pre, const unsigned* __restrict__ wl_count,
+                 const unsigned* __restrict__ wl, const unsigned* __restrict__ lane_mask,
+                 long long cap, int* __restrict__ out_key, long long* __restrict__ out_slot) {
   const int lane = threadIdx.x & 31;
-  const unsigned long long mine = warp_rows[((long long)blockIdx.y * h.nseg + seg) * kPartWarps + warp];
-  if (!mine) return;
-  const long long r0 = (long long)blockIdx.y * kStripRows;
-  const int nr = (int)min((long long)kStripRows, h.rows - r0);
-  // lane i: first output slot of this warp's entries in rows r0 + i and r0 + 32 + i
-  long long first[2] = {0, 0};
+  const unsigned lanes_le = 0xffffffffu >> (31 - lane);
+  const unsigned nitems = *wl_count;
+  const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+  const size_t st = (size_t)h.cols;
+  for (unsigned it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nitems; it += nwarps) {
+    const unsigned unit = wl[it];
+    const long long blk = unit / kPartWarps;
+    const int warp = (int)(unit % kPartWarps);
+    const long long rb = blk / h.nseg;
+    const int seg = (int)(blk - rb * h.nseg);
+    const unsigned long long rows = warp_rows[unit];
+    const unsigned my_lm = lane < 8 ? lane_mask[(long long)unit * 8 + lane] : 0u;
+    // combinations per 8-row group and their running start (every lane holds all 8)
+    int start[9];
+    start[0] = 0;
 #pragma unroll
-  for (int q = 0; q < 2; ++q)
-    if (mine >> (32 * q + lane) & 1) {
-      const long long t = (r0 + 32 * q + lane) * h.nseg + seg;
-      first[q] = tile_off[t] + warp_pre[t * kPartWarps + warp];
+    for (int g = 0; g < 8; ++g) {
+      const unsigned lm = __shfl_sync(0xffffffffu, my_lm, g);
+      start[g + 1] = start[g] + __popc((unsigned)(rows >> (8 * g)) & 0xFFu) * __popc(lm);
     }
-  const long long c0 = (long long)seg * kStripCells + 4 * (warp * 32 + lane);
-  const bool active = c0 < h.cols;
-  strip_rows(h, r0, nr, c0, [&](int i, const int4& up, const int4& cur, const int4& dn, int lf,
-                                int rt) {
-    const long long row_first = __shfl_sync(0xffffffffu, i < 32 ? first[0] : first[1], i & 31);
-    if (!(mine >> i & 1)) return;  // warp-uniform
-    int k[16];
-    const int c = active ? h.keys(up, cur, dn, lf, rt, k) : 0;
-    int incl = c;
+    const int n = start[8];
+    int carry_ri = -1;
+    long long carry = 0;  // entries of row carry_ri placed by the previous iteration
+    for (int g0 = 0; g0 < n; g0 += 32) {
+      const int g = g0 + lane;
+      const bool valid = g < n;
+      int grp = 0;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += u;
-    }
-    if (c) {
-      long long pos = row_first + incl - c;
-      const long long slot0 = ((r0 + i) * h.cols + c0) * 4;
+      for (int q = 1; q < 8; ++q) grp += g >= start[q];
+      const unsigned lm = __shfl_sync(0xffffffffu, my_lm, grp);
+      int ri = 1 << 20;
+      int c = 0;
+      int k[16];
+      long long slot0 = 0, row_first = 0;
+      if (valid) {
+        const int p = __popc(lm);
+        const int local = g - start[grp];
+        const unsigned grows = (unsigned)(rows >> (8 * grp)) & 0xFFu;
+        ri = 8 * grp + (int)__fns(grows, 0, local / p + 1);
+        const int ln = (int)__fns(lm, 0, local % p + 1);
+        const long long r = rb * kStripRows + ri;
+        const long long c0 = (long long)seg * kStripCells + 4 * (warp * 32 + ln);
+        const long long ru = r > 0 ? r - 1 : 0, rd = r + 1 < h.rows ? r + 1 : r;
+        const int4 up = __ldg(reinterpret_cast<const int4*>(h.owner + ru * st + c0));
+        const int4 cur = __ldg(reinterpret_cast<const int4*>(h.owner + r * st + c0));
+        const int4 dn = __ldg(reinterpret_cast<const int4*>(h.owner + rd * st + c0));
+        const int lf = c0 > 0 ? __ldg(h.owner + r * st + c0 - 1) : cur.x;
+        const int rt = c0 + 4 < h.cols ? __ldg(h.owner + r * st + c0 + 4) : cur.w;
+        const long long t = r * h.nseg + seg;
+        row_first = __ldg(tile_off + t) + __ldg(warp_pre + t * kPartWarps + warp);
+        slot0 = (r * h.cols + c0) * 4;
+        c = h.keys(up, cur, dn, lf, rt, k);
+      }
+      int incl = c;
 #pragma unroll
-      for (int s = 0; s < 16; ++s)
-        if (k[s] >= 0) {
-          out_key[pos] = k[s];
-          out_slot[pos] = slot0 + s;
-          ++pos;
-        }
+      for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += u;
+      }
+      // segmented: the first thread of each row's run is a head
+      const int prev_ri = __shfl_up_sync(0xffffffffu, ri, 1);
+      const bool head = lane == 0 || ri != prev_ri;
+      const unsigned heads = __ballot_sync(0xffffffffu, head);
+      const int hl = 31 - __clz(heads & lanes_le);
+      const int seg_base = __shfl_sync(0xffffffffu, incl - c, hl);
+      long long excl = incl - c - seg_base;
+      if (ri == carry_ri) excl += carry;  // the row continues from the previous iteration
+      if (c) {
+        long long pos = row_first + excl;
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (k[q] >= 0) {
+            if (pos < cap) {
+              out_key[pos] = k[q];
+              out_slot[pos] = slot0 + q;
+            }
+            ++pos;
+          }
+      }
+      // carry into the next iteration: the row of lane 31 and what is placed of it so far
+      carry_ri = __shfl_sync(0xffffffffu, ri, 31);
+      carry = __shfl_sync(0xffffffffu, excl + c, 31);
     }
-  });
+  }
+}
+
+// ---- grouping of the compacted entries by (src, dst) pair ---------------------------
+//
+// A stable counting sort of the compacted keys (slot order) with small tiles (1024
+// entries per CTA, so even a few hundred thousand entries fill the GPU): per-tile key
+// histogram, one scan of the key-major [pair][tile] histogram, then a scatter that
+// ranks equal keys within a warp by match.any and across warps / rounds through
+// shared memory, writing each entry's (cell, dim) at its grouped position.
+constexpr int kGroupTile = 4 * kPartThreads;
+
+__global__ void __launch_bounds__(kPartThreads)
+k_group_hist(const int* __restrict__ keys, long long cap, const long long* __restrict__ total,
+             int npairs, long long ntiles, long long* __restrict__ hist) {
+  __shared__ int sh[64];
+  for (int b = threadIdx.x; b < npairs; b += kPartThreads) sh[b] = 0;
+  __syncthreads();
+  const long long n = min(cap, *total);
+  const long long base = (long long)blockIdx.x * kGroupTile;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const long long i = base + q * kPartThreads + threadIdx.x;
+    if (i < n) atomicAdd(&sh[__ldg(keys + i)], 1);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < npairs; b += kPartThreads)
+    hist[(long long)b * ntiles + blockIdx.x] = sh[b];
+}
+
+__global__ void __launch_bounds__(kPartThreads)
+k_group_scatter(const int* __restrict__ keys, const long long* __restrict__ slots, long long cap,
+                const long long* __restrict__ total, int npairs, long long ntiles,
+                const long long* __restrict__ off, int nslots, long long* __restrict__ cells,
+                signed char* __restrict__ dims, const long long* __restrict__ grand,
+                long long* __restrict__ pair_counts, long long* __restrict__ pair_offsets) {
+  __shared__ int wc[kPartWarps][64];
+  __shared__ long long run[64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (blockIdx.x == 0 && threadIdx.x < npairs) {  // k_part_bin_totals, folded in
+    const int b = threadIdx.x;
+    const long long lo = off[(long long)b * ntiles];
+    const long long hi = b + 1 < npairs ? off[(long long)(b + 1) * ntiles] : *grand;
+    pair_counts[b] = hi - lo;
+    pair_offsets[b] = lo;
+  }
+  for (int b = threadIdx.x; b < npairs; b += kPartThreads)
+    run[b] = off[(long long)b * ntiles + blockIdx.x];
+  const long long n = min(cap, *total);
+  const long long base = (long long)blockIdx.x * kGroupTile;
+  const unsigned lt = (1u << lane) - 1;
+  for (int q = 0; q < 4; ++q) {
+    wc[warp][lane] = 0;
+    wc[warp][lane + 32] = 0;
+    __syncwarp();
+    const long long i = base + q * kPartThreads + threadIdx.x;
+    const int key = i < n ? __ldg(keys + i) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (key >= 0 && lane == __ffs(peers) - 1) wc[warp][key] = __popc(peers);
+    __syncthreads();
+    if (key >= 0) {
+      long long pos = run[key] + __popc(peers & lt);
+      for (int w = 0; w < warp; ++w) pos += wc[w][key];
+      const long long sl = __ldg(slots + i);
+      const long long c = sl / nslots;
+      cells[pos] = c;
+      if (dims) dims[pos] = (signed char)(sl - c * nslots);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < npairs; b += kPartThreads) {
+      int add = 0;
+#pragma unroll
+      for (int w = 0; w < kPartWarps; ++w) add += wc[w][b];
+      run[b] += add;
+    }
+    __syncthreads();
+  }
 }
 
 bool make_strip2d(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
@@ -556,51 +705,68 @@ size_t halo_tile_bytes(long long ntiles) {
   return (size_t)(((ntiles * 8 + 255) / 256) * 256) + scan_scratch_bytes(ntiles);
 }
 
-// strip kernels: tile scratch | per-(row block, strip, warp) row masks |
-// per-(tile, warp) first entry (written for non-empty tiles only)
-inline size_t pad256(size_t b) { return (b + 255) / 256 * 256; }
+// strip kernels: tile scratch | per-(row block, strip, warp) row masks | per-(tile, warp)
+// first entry (written for non-empty tiles only) | work list count | work list
 size_t strip_mask_bytes(const Strip2D& h) {
   return pad256((size_t)((h.rows + kStripRows - 1) / kStripRows) * h.nseg * kPartWarps * 8);
 }
+size_t strip_pre_bytes(const Strip2D& h) {
+  return pad256((size_t)h.rows * h.nseg * kPartWarps * 2);
+}
 size_t strip_tile_bytes(const Strip2D& h) {
-  return pad256(halo_tile_bytes(h.rows * h.nseg)) + strip_mask_bytes(h) +
-         (size_t)h.rows * h.nseg * kPartWarps * 2;
+  return pad256(halo_tile_bytes(h.rows * h.nseg)) + strip_mask_bytes(h) + strip_pre_bytes(h) +
+         256 + strip_mask_bytes(h) / 2 + strip_mask_bytes(h) * 4;
 }
 unsigned long long* strip_warp_rows(const Strip2D& h, void* scratch) {
   return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(scratch) +
-                                     pad256(halo_tile_bytes(h.rows * h.nseg)));
+                                               pad256(halo_tile_bytes(h.rows * h.nseg)));
 }
 unsigned short* strip_warp_pre(const Strip2D& h, void* scratch) {
   return reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(strip_warp_rows(h, scratch)) +
                                            strip_mask_bytes(h));
 }
+unsigned* strip_wl_count(const Strip2D& h, void* scratch) {
+  return reinterpret_cast<unsigned*>(reinterpret_cast<char*>(strip_warp_pre(h, scratch)) +
+                                     strip_pre_bytes(h));
+}
+unsigned* strip_wl(const Strip2D& h, void* scratch) { return strip_wl_count(h, scratch) + 64; }
+unsigned* strip_lane_mask(const Strip2D& h, void* scratch) {
+  return reinterpret_cast<unsigned*>(reinterpret_cast<char*>(strip_wl(h, scratch)) +
+                                     strip_mask_bytes(h) / 2);
+}
 
 template <class Key>
 int halo_count(const Key& key, long long n, int npairs, long long* pair_cnt, void* scratch,
-               size_t bytes, cudaStream_t s) {
+               size_t bytes, long long* total_out, cudaStream_t s) {
   const long long ntiles = (n + kHaloTile - 1) / kHaloTile;
   if (bytes < halo_tile_bytes(ntiles)) return set_error("pm_halo_count: scratch too small"),
                                                PM_ERR_INVALID;
   PM_CUDA_TRY(cudaMemsetAsync(pair_cnt, 0, sizeof(long long) * npairs, s));
-  if (ntiles == 0) return PM_OK;
+  if (ntiles == 0) {
+    if (total_out) PM_CUDA_TRY(cudaMemsetAsync(total_out, 0, 8, s));
+    return PM_OK;
+  }
   long long* tile = reinterpret_cast<long long*>(scratch);
   void* scan_tmp = reinterpret_cast<char*>(scratch) + ((ntiles * 8 + 255) / 256) * 256;
   k_halo_count<Key><<<(unsigned)ntiles, kPartThreads, sizeof(int) * npairs, s>>>(
       key, n, npairs, tile, reinterpret_cast<unsigned long long*>(pair_cnt));
   PM_CUDA_TRY(cudaGetLastError());
-  return exclusive_scan_i64(tile, ntiles, scan_tmp, s);
+  int rc = exclusive_scan_i64(tile, ntiles, scan_tmp, s);
+  if (rc || !total_out) return rc;
+  PM_CUDA_TRY(cudaMemcpyAsync(total_out, scan_tmp, 8, cudaMemcpyDeviceToDevice, s));
+  return PM_OK;
 }
 
 template <class Key>
 int halo_compact(const Key& key, long long n, void* scratch, int* keys, long long* slots_out,
-                 cudaStream_t s) {
+                 long long cap, cudaStream_t s) {
   const long long ntiles = (n + kHaloTile - 1) / kHaloTile;
   if (ntiles == 0) return PM_OK;
   const long long* tile = reinterpret_cast<const long long*>(scratch);
   const long long* total = reinterpret_cast<const long long*>(
       reinterpret_cast<char*>(scratch) + ((ntiles * 8 + 255) / 256) * 256);
-  k_halo_compact<Key><<<(unsigned)ntiles, kPartThreads, 0, s>>>(key, n, ntiles, tile, total, keys,
-                                                               slots_out);
+  k_halo_compact<Key><<<(unsigned)ntiles, kPartThreads, 0, s>>>(key, n, ntiles, tile, total, cap,
+                                                               keys, slots_out);
   PM_CUDA_TRY(cudaGetLastError());
   return PM_OK;
 }
@@ -660,7 +826,7 @@ size_t pm_halo_tile_scratch_bytes(const int64_t* ext, int32_t rank) {
 
 int pm_halo_count(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
                   int32_t nprocs, int64_t* pair_counts, void* tile_scratch, size_t bytes,
-                  void* stream) {
+                  int64_t* total, void* stream) {
   long long ncells = 0;
   pm::HaloKey<unsigned long long> key64;
   if (!owner || !pair_counts || !tile_scratch ||
@@ -676,29 +842,33 @@ int pm_halo_count(const int32_t* owner, const int64_t* ext, int32_t rank, const 
       return pm::set_error("pm_halo_count: scratch too small"), PM_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     PM_CUDA_TRY(cudaMemsetAsync(pc, 0, sizeof(long long) * nprocs * nprocs, s));
+    PM_CUDA_TRY(cudaMemsetAsync(pm::strip_wl_count(h2, tile_scratch), 0, 4, s));
     long long* tile = reinterpret_cast<long long*>(tile_scratch);
     const dim3 grid((unsigned)h2.nseg, (unsigned)((h2.rows + pm::kStripRows - 1) / pm::kStripRows));
     pm::k_halo2d_count<<<grid, pm::kPartThreads, sizeof(int) * nprocs * nprocs, s>>>(
         h2, nprocs * nprocs, tile, reinterpret_cast<unsigned long long*>(pc),
-        pm::strip_warp_rows(h2, tile_scratch), pm::strip_warp_pre(h2, tile_scratch));
+        pm::strip_warp_rows(h2, tile_scratch), pm::strip_warp_pre(h2, tile_scratch),
+        pm::strip_wl_count(h2, tile_scratch), pm::strip_wl(h2, tile_scratch),
+        pm::strip_lane_mask(h2, tile_scratch));
     PM_CUDA_TRY(cudaGetLastError());
-    return pm::exclusive_scan_i64(tile, ntiles,
-                                  reinterpret_cast<char*>(tile_scratch) +
-                                      ((ntiles * 8 + 255) / 256) * 256,
-                                  s);
+    void* scan_tmp = reinterpret_cast<char*>(tile_scratch) + ((ntiles * 8 + 255) / 256) * 256;
+    int rc = pm::exclusive_scan_i64(tile, ntiles, scan_tmp, s);
+    if (rc || !total) return rc;
+    PM_CUDA_TRY(cudaMemcpyAsync(total, scan_tmp, 8, cudaMemcpyDeviceToDevice, s));
+    return PM_OK;
   }
   if (items <= (1LL << 32)) {
     pm::HaloKey<unsigned> key32;
     pm::make_key(owner, ext, rank, halo, nprocs, &key32, &ncells);
     return pm::halo_count(key32, items, nprocs * nprocs, pc, tile_scratch, bytes,
-                          (cudaStream_t)stream);
+                          reinterpret_cast<long long*>(total), (cudaStream_t)stream);
   }
   return pm::halo_count(key64, items, nprocs * nprocs, pc, tile_scratch, bytes,
-                        (cudaStream_t)stream);
+                        reinterpret_cast<long long*>(total), (cudaStream_t)stream);
 }
 
 int pm_halo_compact(const int32_t* owner, const int64_t* ext, int32_t rank, const int32_t* halo,
-                    int32_t nprocs, void* tile_scratch, int32_t* keys, int64_t* slots,
+                    int32_t nprocs, void* tile_scratch, int32_t* keys, int64_t* slots, int64_t cap,
                     void* stream) {
   long long ncells = 0;
   pm::HaloKey<unsigned long long> key64;
@@ -710,21 +880,64 @@ int pm_halo_compact(const int32_t* owner, const int64_t* ext, int32_t rank, cons
   pm::Strip2D h2;
   if (pm::make_strip2d(owner, ext, rank, halo, nprocs, &h2)) {
     const long long* tile = reinterpret_cast<const long long*>(tile_scratch);
-    // one warp per CTA; warps without entries return after reading their row mask
-    const dim3 grid((unsigned)(h2.nseg * pm::kPartWarps),
-                    (unsigned)((h2.rows + pm::kStripRows - 1) / pm::kStripRows));
-    pm::k_halo2d_compact<<<grid, 32, 0, (cudaStream_t)stream>>>(
+    // persistent warps over the work list
+    pm::k_halo2d_compact<<<(unsigned)(pm::num_sms() * 8), 256, 0, (cudaStream_t)stream>>>(
         h2, tile, pm::strip_warp_rows(h2, tile_scratch), pm::strip_warp_pre(h2, tile_scratch),
-        keys, so);
+        pm::strip_wl_count(h2, tile_scratch), pm::strip_wl(h2, tile_scratch),
+        pm::strip_lane_mask(h2, tile_scratch), cap, keys, so);
     PM_CUDA_TRY(cudaGetLastError());
     return PM_OK;
   }
   if (items <= (1LL << 32)) {
     pm::HaloKey<unsigned> key32;
     pm::make_key(owner, ext, rank, halo, nprocs, &key32, &ncells);
-    return pm::halo_compact(key32, items, tile_scratch, keys, so, (cudaStream_t)stream);
+    return pm::halo_compact(key32, items, tile_scratch, keys, so, cap, (cudaStream_t)stream);
   }
-  return pm::halo_compact(key64, items, tile_scratch, keys, so, (cudaStream_t)stream);
+  return pm::halo_compact(key64, items, tile_scratch, keys, so, cap, (cudaStream_t)stream);
+}
+
+size_t pm_halo_group_scratch_bytes(int64_t cap, int32_t nprocs) {
+  const long long ntiles = (cap + pm::kGroupTile - 1) / pm::kGroupTile;
+  const long long len = std::max(1LL, ntiles * nprocs * nprocs);
+  return pm::pad256((size_t)len * 8) + pm::scan_scratch_bytes(len);
+}
+
+int pm_halo_group(const int32_t* keys, const int64_t* slots, int64_t cap, const int64_t* total,
+                  int32_t rank, int32_t nprocs, int64_t* pair_counts, int64_t* pair_offsets,
+                  int64_t* cells, int8_t* dims, void* scratch, size_t scratch_bytes,
+                  void* stream) {
+  if (cap < 0 || rank < 1 || rank > 3 || nprocs < 1 || nprocs > 8 || !total || !pair_counts ||
+      !pair_offsets || !scratch || (cap > 0 && (!keys || !slots || !cells)))
+    return pm::set_error("pm_halo_group: bad arguments (nprocs 1..8)"), PM_ERR_INVALID;
+  if (scratch_bytes < pm_halo_group_scratch_bytes(cap, nprocs))
+    return pm::set_error("pm_halo_group: scratch too small"), PM_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int npairs = nprocs * nprocs;
+  const long long ntiles = std::max(1LL, (long long)((cap + pm::kGroupTile - 1) / pm::kGroupTile));
+  const long long len = ntiles * npairs;
+  long long* hist = reinterpret_cast<long long*>(scratch);
+  void* scan_tmp = reinterpret_cast<char*>(scratch) + pm::pad256((size_t)len * 8);
+  auto* tot = reinterpret_cast<const long long*>(total);
+  pm::k_group_hist<<<(unsigned)ntiles, pm::kPartThreads, 0, s>>>(keys, cap, tot, npairs, ntiles,
+                                                                hist);
+  PM_CUDA_TRY(cudaGetLastError());
+  int rc = pm::exclusive_scan_i64(hist, len, scan_tmp, s);
+  if (rc) return rc;
+  if (cells) {  // the scatter's block 0 also writes the per-pair counts / offsets
+    pm::k_group_scatter<<<(unsigned)ntiles, pm::kPartThreads, 0, s>>>(
+        keys, reinterpret_cast<const long long*>(slots), cap, tot, npairs, ntiles, hist, 2 * rank,
+        reinterpret_cast<long long*>(cells), reinterpret_cast<signed char*>(dims),
+        reinterpret_cast<const long long*>(scan_tmp), reinterpret_cast<long long*>(pair_counts),
+        reinterpret_cast<long long*>(pair_offsets));
+    PM_CUDA_TRY(cudaGetLastError());
+    return PM_OK;
+  }
+  pm::k_part_bin_totals<<<1, 64, 0, s>>>(hist, ntiles, npairs,
+                                         reinterpret_cast<const long long*>(scan_tmp),
+                                         reinterpret_cast<long long*>(pair_counts),
+                                         reinterpret_cast<long long*>(pair_offsets));
+  PM_CUDA_TRY(cudaGetLastError());
+  return PM_OK;
 }
 
 int pm_halo_gather(const int32_t* perm, const int64_t* slots, int64_t n, int32_t rank,

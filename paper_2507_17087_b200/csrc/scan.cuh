@@ -84,6 +84,41 @@ k_scan_apply(long long* __restrict__ x, long long len, const long long* __restri
   if (grand_total && threadIdx.x == 0) *grand_total = total;
 }
 
+// Apply pass that finds its own block offset: the sum of the block sums before it
+// (read straight from L2 -- at most kScanLookback of them), so a scan of up to
+// kScanBlock * kScanLookback elements is two launches with no recursion; the last
+// block writes the grand total.
+constexpr long long kScanLookback = 4096;
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_apply_lb(long long* __restrict__ x, long long len, const long long* __restrict__ sums,
+                long long* __restrict__ grand_total) {
+  __shared__ long long s_off;
+  long long pre = 0;
+  for (long long b = threadIdx.x; b < blockIdx.x; b += kScanThreads) pre += __ldg(sums + b);
+  long long dummy;
+  pre = block_excl_scan(pre, &dummy);  // the block-wide sum lands in dummy
+  if (threadIdx.x == 0) s_off = dummy;
+  __syncthreads();
+  const long long off = s_off;
+  const long long base = blockIdx.x * kScanBlock + (long long)threadIdx.x * kScanItems;
+  long long v[kScanItems];
+  long long sm = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    v[j] = (base + j < len) ? x[base + j] : 0;
+    sm += v[j];
+  }
+  long long total;
+  long long run = block_excl_scan(sm, &total) + off;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    if (base + j < len) x[base + j] = run;
+    run += v[j];
+  }
+  if (threadIdx.x == 0 && blockIdx.x == gridDim.x - 1) *grand_total = off + total;
+}
+
 // In-place exclusive scan; the grand total lands in *(long long*)scratch.
 inline int exclusive_scan_i64(long long* x, long long len, void* scratch, cudaStream_t s) {
   long long* total = reinterpret_cast<long long*>(scratch);
@@ -102,6 +137,11 @@ inline int exclusive_scan_i64(long long* x, long long len, void* scratch, cudaSt
   cur += nblk * 8 + 64;
   k_scan_reduce<<<(unsigned)nblk, kScanThreads, 0, s>>>(x, len, sums);
   PM_CUDA_TRY(cudaGetLastError());
+  if (nblk <= kScanLookback) {
+    k_scan_apply_lb<<<(unsigned)nblk, kScanThreads, 0, s>>>(x, len, sums, total);
+    PM_CUDA_TRY(cudaGetLastError());
+    return PM_OK;
+  }
   // recurse: scan the block sums, total goes to the same grand-total slot
   {
     // the recursive call needs its own total slot followed by its levels; we

@@ -54,9 +54,12 @@ SIGNATURES = {
                                      _I32, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
     "pm_halo_tile_scratch_bytes": (ctypes.c_size_t, [ctypes.POINTER(_I64), _I32]),
     "pm_halo_count": (ctypes.c_int, [_VP, ctypes.POINTER(_I64), _I32, ctypes.POINTER(_I32),
-                                     _I32, _VP, _VP, _SZ, _VP]),
+                                     _I32, _VP, _VP, _SZ, _VP, _VP]),
     "pm_halo_compact": (ctypes.c_int, [_VP, ctypes.POINTER(_I64), _I32, ctypes.POINTER(_I32),
-                                       _I32, _VP, _VP, _VP, _VP]),
+                                       _I32, _VP, _VP, _VP, _I64, _VP]),
+    "pm_halo_group_scratch_bytes": (_SZ, [_I64, _I32]),
+    "pm_halo_group": (ctypes.c_int, [_VP, _VP, _I64, _VP, _I32, _I32, _VP, _VP, _VP, _VP, _VP,
+                                     _SZ, _VP]),
     "pm_halo_gather": (ctypes.c_int, [_VP, _VP, _I64, _I32, _VP, _VP, _VP]),
     "pm_gemm_bf16": (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _I32,
                                     _I32, _VP]),

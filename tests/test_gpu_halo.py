@@ -184,3 +184,32 @@ def test_strip_2d_out_of_range_owners_match_single_call(cuda, ext, P):
     assert torch.equal(counts, want.pair_counts)
     assert torch.equal(offsets, want.pair_offsets)
     assert torch.equal(cells[:total], want.cells) and torch.equal(dims[:total], want.dims)
+
+
+@pytest.mark.parametrize("ext,P", [((256, 1024), 8), ((77, 96), 6), ((9, 10, 11), 5)])
+def test_capacity_mode_matches_exact(cuda, ext, P):
+    """capacity= (no host round trip inside the call) gives the exact lists when the
+    capacity suffices, and raises on access when it does not; repeated calls on one
+    stream share the workspace without corrupting earlier results."""
+    from paper_2507_17087_b200.errors import ProcMapError
+
+    torch = cuda
+    g = torch.Generator(device="cuda").manual_seed(sum(ext) * 7 + P)
+    n = 1
+    for e in ext:
+        n *= e
+    halo = (1,) * len(ext)
+    owner = torch.randint(0, P, (n,), device="cuda", dtype=torch.int32, generator=g)
+    owner2 = torch.randint(0, P, (n,), device="cuda", dtype=torch.int32, generator=g)
+    want = halo_lists(owner, ext, halo, P)
+    want2 = halo_lists(owner2, ext, halo, P)
+    a = halo_lists(owner, ext, halo, P, capacity=want.total + 17)
+    b = halo_lists(owner2, ext, halo, P, capacity=max(want.total, want2.total))
+    for got, ref in ((a, want), (b, want2)):
+        assert got.total == ref.total
+        assert torch.equal(got.pair_counts, ref.pair_counts)
+        assert torch.equal(got.pair_offsets, ref.pair_offsets)
+        assert torch.equal(got.cells, ref.cells) and torch.equal(got.dims, ref.dims)
+    small = halo_lists(owner, ext, halo, P, capacity=max(0, want.total - 1))
+    with pytest.raises(ProcMapError):
+        small.total
