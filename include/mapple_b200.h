@@ -346,10 +346,7 @@ typedef struct pm_hydro_view {
   float* zpe;                /* p + q of the last step (0 before the first)    */
   const float* pm;           /* [n_points] point mass                          */
   const int8_t* pbc;         /* [n_points] wall flags                          */
-  float* px[PM_HYDRO_MAX_RANKS];
-  float* py[PM_HYDRO_MAX_RANKS];
-  float* ux[PM_HYDRO_MAX_RANKS];
-  float* uy[PM_HYDRO_MAX_RANKS];
+  float* pst[PM_HYDRO_MAX_RANKS];     /* per point (x, y, u, v): 16 bytes  */
   float* fxy[PM_HYDRO_MAX_RANKS];     /* interleaved (fx, fy) per point  */
   int32_t rank;
   float dt, gamma, cq;

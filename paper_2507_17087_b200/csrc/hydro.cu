@@ -3,9 +3,9 @@
 // quadrilateral mesh, with the shared-point exchange fused over NVLink.
 //
 // Zones are placed by a Mapple mapping of the zone launch; each point belongs
-// to one GPU.  A zone reads its 4 points' positions and velocities through
-// per-rank pointer tables (peer loads over NVLink for points owned by another
-// GPU) and deposits its corner forces with 8-byte float2 atomics straight into the
+// to one GPU.  A zone reads its 4 points' state -- (x, y, u, v), one 16-byte
+// record per point -- through per-rank pointer tables (peer loads over NVLink for
+// points owned by another GPU) and deposits its corner forces with 8-byte float2 atomics straight into the
 // owning GPU's force array -- Legion PENNANT's master/ghost point exchange
 // and its point-force reduction become the cross-GPU corners of the zone
 // kernel, with no copy pass.
@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "pm_common.h"
 
@@ -45,14 +46,16 @@ k_hydro_zones(const __grid_constant__ HydroArgs a) {
   float x[4], y[4], u[4], w[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) ref[k] = __ldg(v.z2p + k * nz + z);
-  // point state is read-only during this phase (also on the peers): non-coherent loads
+  // point state is read-only during this phase (also on the peers): one 16-byte
+  // non-coherent load of (x, y, u, v) per corner
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int r = rk(ref[k]), s = sl(ref[k]);
-    x[k] = __ldg(v.px[r] + s);
-    y[k] = __ldg(v.py[r] + s);
-    u[k] = __ldg(v.ux[r] + s);
-    w[k] = __ldg(v.uy[r] + s);
+    const float4 q = __ldg(reinterpret_cast<const float4*>(v.pst[r]) + s);
+    x[k] = q.x;
+    y[k] = q.y;
+    u[k] = q.z;
+    w[k] = q.w;
   }
   float area = 0.f, dadt = 0.f;
   float nx[4], ny[4];  // edge k (point k -> k+1) outward normal scaled by its length
@@ -94,63 +97,37 @@ k_hydro_zones(const __grid_constant__ HydroArgs a) {
   }
 }
 
+__device__ __forceinline__ float4 hydro_move(float4 q, float2 f, float m, int bc, float dt) {
+  const float rm = 1.0f / m;
+  const float ax = (bc & 1) ? 0.f : f.x * rm;
+  const float ay = (bc & 2) ? 0.f : f.y * rm;
+  const float u1 = q.z + dt * ax, w1 = q.w + dt * ay;
+  return make_float4(q.x + dt * 0.5f * (q.z + u1), q.y + dt * 0.5f * (q.w + w1), u1, w1);
+}
+
 __global__ void __launch_bounds__(256)
 k_hydro_points(const __grid_constant__ HydroArgs a) {
   const pm_hydro_view& v = a.v;
   const int me = v.rank;
-  float *px = v.px[me], *py = v.py[me], *ux = v.ux[me], *uy = v.uy[me];
+  float4* st = reinterpret_cast<float4*>(v.pst[me]);
   float2* f = reinterpret_cast<float2*>(v.fxy[me]);
   const float dt = v.dt;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  // four points per thread: 16-byte loads / stores of every array (all base
-  // pointers are 16-byte aligned allocations; the tail goes point by point)
-  const long long nv = v.n_points >> 2;
+  // two points per thread: 16-byte accesses to every array but the masses (8 bytes) and
+  // the wall flags (2 bytes); the tail goes point by point
+  const long long nv = v.n_points >> 1;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < nv; g += stride) {
-    const float4 m4 = __ldg(reinterpret_cast<const float4*>(v.pm) + g);
-    const char4 b4 = __ldg(reinterpret_cast<const char4*>(v.pbc) + g);
-    const float4 fa = reinterpret_cast<const float4*>(f)[2 * g];      // fx0 fy0 fx1 fy1
-    const float4 fb = reinterpret_cast<const float4*>(f)[2 * g + 1];  // fx2 fy2 fx3 fy3
-    float4 u = reinterpret_cast<float4*>(ux)[g], w = reinterpret_cast<float4*>(uy)[g];
-    float4 x = reinterpret_cast<float4*>(px)[g], y = reinterpret_cast<float4*>(py)[g];
-    const float fxs[4] = {fa.x, fa.z, fb.x, fb.z}, fys[4] = {fa.y, fa.w, fb.y, fb.w};
-    const float ms[4] = {m4.x, m4.y, m4.z, m4.w};
-    const int bcs[4] = {b4.x, b4.y, b4.z, b4.w};
-    float* uu = &u.x;
-    float* ww = &w.x;
-    float* xx = &x.x;
-    float* yy = &y.x;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float rm = 1.0f / ms[j];
-      const float ax = (bcs[j] & 1) ? 0.f : fxs[j] * rm;
-      const float ay = (bcs[j] & 2) ? 0.f : fys[j] * rm;
-      const float u1 = uu[j] + dt * ax, w1 = ww[j] + dt * ay;
-      xx[j] += dt * 0.5f * (uu[j] + u1);
-      yy[j] += dt * 0.5f * (ww[j] + w1);
-      uu[j] = u1;
-      ww[j] = w1;
-    }
-    reinterpret_cast<float4*>(ux)[g] = u;
-    reinterpret_cast<float4*>(uy)[g] = w;
-    reinterpret_cast<float4*>(px)[g] = x;
-    reinterpret_cast<float4*>(py)[g] = y;
-    reinterpret_cast<float4*>(f)[2 * g] = make_float4(0.f, 0.f, 0.f, 0.f);
-    reinterpret_cast<float4*>(f)[2 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float2 m2 = __ldg(reinterpret_cast<const float2*>(v.pm) + g);
+    const char2 b2 = __ldg(reinterpret_cast<const char2*>(v.pbc) + g);
+    const float4 ff = __ldcs(reinterpret_cast<const float4*>(f) + g);  // fx0 fy0 fx1 fy1
+    const float4 q0 = st[2 * g], q1 = st[2 * g + 1];
+    st[2 * g] = hydro_move(q0, make_float2(ff.x, ff.y), m2.x, b2.x, dt);
+    st[2 * g + 1] = hydro_move(q1, make_float2(ff.z, ff.w), m2.y, b2.y, dt);
+    reinterpret_cast<float4*>(f)[g] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  for (long long n = 4 * nv + (long long)blockIdx.x * blockDim.x + threadIdx.x; n < v.n_points;
+  for (long long n = 2 * nv + (long long)blockIdx.x * blockDim.x + threadIdx.x; n < v.n_points;
        n += stride) {
-    const float rm = 1.0f / v.pm[n];
-    const int bc = v.pbc[n];
-    const float2 fn = f[n];
-    float ax = fn.x * rm, ay = fn.y * rm;
-    if (bc & 1) ax = 0.f;
-    if (bc & 2) ay = 0.f;
-    const float u0 = ux[n], w0 = uy[n];
-    const float u1 = u0 + dt * ax, w1 = w0 + dt * ay;
-    px[n] += dt * 0.5f * (u0 + u1);
-    py[n] += dt * 0.5f * (w0 + w1);
-    ux[n] = u1;
-    uy[n] = w1;
+    st[n] = hydro_move(st[n], f[n], v.pm[n], v.pbc[n], dt);
     f[n] = make_float2(0.f, 0.f);
   }
 }
@@ -173,9 +150,12 @@ int pm_hydro_step(const pm_hydro_view* view, int32_t phase, void* stream) {
     pm::k_hydro_zones<<<(unsigned)((view->n_zones + 255) / 256), 256, 0, s>>>(a);
   } else if (phase == 1) {
     if (view->n_points == 0) return PM_OK;
-    long long blocks = (view->n_points / 4 + 255) / 256 + 1;
-    const long long cap = (long long)pm::num_sms() * 8;
-    if (blocks > cap) blocks = cap;
+    // one thread per two points, no grid-stride persistence (0.53 vs 0.61 ms at 67M
+    // points with 8 CTAs per SM looping)
+    long long blocks = (view->n_points / 2 + 255) / 256 + 1;
+    if (const char* c = getenv("PM_HYDRO_POINT_CTAS"))
+      if (atoll(c) > 0 && atoll(c) < blocks) blocks = atoll(c);
+    if (blocks > 0x7FFFFFFFLL) blocks = 0x7FFFFFFFLL;
     pm::k_hydro_points<<<(unsigned)blocks, 256, 0, s>>>(a);
   } else {
     return pm::set_error("pm_hydro_step: phase 0 (zones) or 1 (points)"), PM_ERR_INVALID;

@@ -54,7 +54,7 @@ class PmHydroView(ctypes.Structure):
                 ("z2p", ctypes.c_void_p), ("zm", ctypes.c_void_p), ("ze", ctypes.c_void_p),
                 ("za", ctypes.c_void_p), ("zpe", ctypes.c_void_p), ("pm", ctypes.c_void_p),
                 ("pbc", ctypes.c_void_p)] + \
-               [(n, ctypes.c_void_p * MAX_RANKS) for n in ("px", "py", "ux", "uy", "fxy")] + \
+               [(n, ctypes.c_void_p * MAX_RANKS) for n in ("pst", "fxy")] + \
                [("rank", ctypes.c_int32), ("dt", ctypes.c_float), ("gamma", ctypes.c_float),
                 ("cq", ctypes.c_float)]
 
@@ -107,29 +107,29 @@ class MappedHydro:
         self.zpe = torch.zeros(nz, dtype=torch.float32, device=dev)
         # points
         gj, gi = self.point_ids // W, self.point_ids % W
-        self.px = (gi.to(torch.float64) / Lx).to(torch.float32)
-        self.py = (gj.to(torch.float64) / Ly).to(torch.float32)
-        self.ux = torch.zeros_like(self.px)
-        self.uy = torch.zeros_like(self.px)
-        self.fxy = torch.zeros(2 * max(self.px.numel(), 1), dtype=torch.float32, device=dev)
+        # point state (x, y, u, v) as one 16-byte record per point (a zone gathers each
+        # corner with one vector load); px / py / ux / uy are strided views of it
+        npl = self.point_ids.numel()
+        self.pst = torch.zeros(max(npl, 1), 4, dtype=torch.float32, device=dev)
+        self.pst[:npl, 0] = (gi.to(torch.float64) / Lx).to(torch.float32)
+        self.pst[:npl, 1] = (gj.to(torch.float64) / Ly).to(torch.float32)
+        self.px, self.py, self.ux, self.uy = (self.pst[:, c] for c in range(4))
+        self.fxy = torch.zeros(2 * max(npl, 1), dtype=torch.float32, device=dev)
         nadj = ((gi > 0).to(i64) + (gi < Lx).to(i64)) * ((gj > 0).to(i64) + (gj < Ly).to(i64))
         self.pm = (nadj.to(torch.float64) * h2 / 4.0).to(torch.float32)
         self.pbc = (((gi == 0) | (gi == Lx)).to(torch.int8) +
                     2 * ((gj == 0) | (gj == Ly)).to(torch.int8)).contiguous()
-        if self.px.numel() == 0:  # a GPU without points still exposes 1-element arrays
-            for n in ("px", "py", "ux", "uy"):
-                setattr(self, n, torch.zeros(1, dtype=torch.float32, device=dev))
         # the communication model: corners whose point lives on another GPU
         self.cross_corners = int(((self.z2p.to(i64) >> 27) != rank).sum())
-        self.peers = PeerBuffers({n: getattr(self, n) for n in ("px", "py", "ux", "uy", "fxy")},
-                                 rank, world, group)
+        self.peers = PeerBuffers({n: getattr(self, n) for n in ("pst", "fxy")}, rank, world,
+                                 group)
         v = PmHydroView()
         v.n_zones, v.n_points = nz, self.point_ids.numel()
         v.z2p, v.zm, v.ze, v.za, v.zpe = (self.z2p.data_ptr(), self.zm.data_ptr(),
                                           self.ze.data_ptr(), self.za.data_ptr(),
                                           self.zpe.data_ptr())
         v.pm, v.pbc = self.pm.data_ptr(), self.pbc.data_ptr()
-        for n in ("px", "py", "ux", "uy", "fxy"):
+        for n in ("pst", "fxy"):
             arr = getattr(v, n)
             for r in range(world):
                 arr[r] = self.peers.ptrs[n][r]
@@ -159,7 +159,8 @@ class MappedHydro:
         native.check(lib.pm_hydro_step(ctypes.byref(self.view), 1, cs), "pm_hydro_step")
 
     # algorithmic HBM bytes per zone-step: zone kernel 16 (z2p) + 16 (zm, ze, za, zpe) +
-    # 12 (ze, za, zpe) + 16 (point x, y, u, v) + 8 (force RMW); point kernel 29 read + 24 write
+    # 12 (ze, za, zpe) + 16 (point x, y, u, v) + 8 (force RMW); point kernel 29 read
+    # (state 16, force 8, mass 4, wall flags 1) + 24 write (state 16, force reset 8)
     BYTES_PER_ZONE_STEP = 16 + 16 + 12 + 16 + 8 + 29 + 24
 
     def close(self):
