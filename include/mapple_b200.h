@@ -289,6 +289,10 @@ typedef struct pm_stencil_view {
   int32_t* nbr_flag_slot[4]; /* &neighbour.my_flags[my rank] (peer pointers)   */
   int32_t nbr_rank[4];
   uint32_t* ticket;          /* unused (kept for the struct layout)           */
+  float* col_out[2];         /* my first / last column of `out`, contiguous    */
+                             /* (read by the left / right neighbour)           */
+  const float* nbr_col[2];   /* left neighbour's last column of its `in` strip,*/
+                             /* right neighbour's first column (peer pointers) */
 } pm_stencil_view;
 int pm_stencil_sweep(const pm_stencil_view* view, int32_t sweep, void* stream);
 

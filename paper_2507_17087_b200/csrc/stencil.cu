@@ -9,19 +9,28 @@
 // neighbouring GPU's `in` buffer over NVLink (peer pointers, L2-bypassing
 // loads) -- no halo buffers, no copies, no NCCL.
 //
+// Left / right neighbours exchange columns through column strips: the first and
+// last column of every rectangle are computed by dedicated CTAs (launched last) that
+// read the neighbour's adjacent column as a contiguous strip -- 16-byte NVLink loads
+// of 4 rows -- and publish their own column into a strip for the next sweep, so no
+// tile waits on a left / right neighbour and no tile does per-row scalar peer loads.
+//
 // Cross-GPU ordering, per neighbour (flags pushed into the reader's memory; flag =
 // sweeps the writer has completed):
 //   publish  sweep s's kernel starts only after all CTAs of sweep s-1 finished
 //            (stream order), so its first CTA publishes "s sweeps done" with a
 //            system-scope release store into each neighbour's flag slot -- no
 //            per-CTA ticket atomics or fences;
-//   RAW      a tile touching my rectangle's edge waits until that neighbour
-//            has published s (finished sweep s-1); interior tiles never wait;
-//   WAR      with three rotating buffers a neighbour reads the buffer I write
-//            at sweep s during its sweep s-2.  My sweep s-1 edge tiles on that
-//            side already waited for the neighbour's flag >= s-1, i.e. for its
-//            sweep s-2 to finish, so the WAR order is implied and not checked.
-// Tiles are launched interior-first so edge tiles usually find the flag set.
+//   RAW      a first / last row tile waits until the up / down neighbour has
+//            published s (finished sweep s-1), a column-strip CTA until every
+//            neighbour has; other tiles never wait;
+//   WAR      with three rotating buffers (and column strips) a neighbour reads
+//            the buffer / strip I write at sweep s during its sweep s-2.  My
+//            sweep s-1 row-edge tiles (up / down) or strip CTAs (left / right)
+//            already waited for that neighbour's flag >= s-1, i.e. for its sweep
+//            s-2 to finish, so the WAR order is implied and not checked.
+// Launch order: column-strip CTAs, the middle tile rows, then the first / last tile
+// rows, so the tiles that wait on flags usually find them set.
 //
 // Traffic: 8 B per cell per sweep from HBM (read in, write out); vertical
 // neighbours are reused through L1 inside a 16-row tile.
@@ -56,6 +65,13 @@ __device__ __forceinline__ float ld_peer(const float* p) {
   return v;
 }
 
+__device__ __forceinline__ float4 ld_peer4(const float* p) {
+  float4 v;
+  asm volatile("ld.relaxed.sys.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void wait_flag(const int32_t* f, int target) {
   if (ld_acquire_sys(f) >= target) return;
   while (ld_acquire_sys(f) < target) __nanosleep(256);
@@ -70,51 +86,104 @@ __device__ __forceinline__ float fetch(const pm_stencil_view& v, int64_t i, int6
   return ld_peer(v.nbr[3] + i * v.nbr_pitch[3]);
 }
 
-template <int TR>
-__global__ void __launch_bounds__(kThreads)
-k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_interior) {
-  // interior tiles first, edge tiles last (block index order = launch order)
-  const int b = blockIdx.x;
-  int tr, tc;
-  if (b < n_interior) {
-    const int ic = tiles_c - 2;
-    tr = 1 + b / ic;
-    tc = 1 + b % ic;
-  } else {
-    // the ring of edge tiles: top row, bottom row, then left/right of the rest
-    int e = b - n_interior;
-    const int per_mid = tiles_c > 1 ? 2 : 1;
-    if (e < tiles_c) {
-      tr = 0;
-      tc = e;
-    } else if (tiles_r > 1 && e < 2 * tiles_c) {
-      tr = tiles_r - 1;
-      tc = e - tiles_c;
+// The first / last column of the rectangle when a left / right neighbour exists: one
+// thread per 4 rows reads the neighbour's published column strip with one 16-byte
+// NVLink load, computes the 4 cells and publishes them into its own strip for the
+// next sweep.  These CTAs (launched after every tile) are the only ones that wait for
+// the left / right neighbours; the tiles leave those cells to them.
+constexpr int kStripRowsPerCta = 4 * kThreads;
+#ifndef PM_STRIPS_FIRST
+#define PM_STRIPS_FIRST 1
+#endif
+
+__device__ __noinline__ void column_strip(const pm_stencil_view& v, int sweep, int side, int blk) {
+  if (threadIdx.x == 0 && sweep > 0) {
+    for (int d = 0; d < 4; ++d)
+      if (v.nbr[d]) wait_flag(v.my_flags + v.nbr_rank[d], sweep);
+  }
+  __syncthreads();
+  const int64_t i0 = (int64_t)blk * kStripRowsPerCta + 4 * threadIdx.x;
+  if (i0 >= v.rows) return;
+  const int64_t j = side ? v.cols - 1 : 0;
+  const float4 nb = ld_peer4(v.nbr_col[side] + i0);  // the neighbour's adjacent column
+  const float nbv[4] = {nb.x, nb.y, nb.z, nb.w};
+  float res[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t i = i0 + q;
+    if (i >= v.rows) break;
+    const int64_t gi = v.grow0 + i;
+    const float mid = __ldg(v.in + i * v.pitch + j);
+    if (gi == 0 || gi == v.grows - 1) {
+      res[q] = mid;  // Dirichlet row
     } else {
-      e -= (tiles_r > 1 ? 2 : 1) * tiles_c;
-      tr = 1 + e / per_mid;
-      tc = (e % per_mid == 0) ? 0 : tiles_c - 1;
+      const float up = fetch(v, i - 1, j), dn = fetch(v, i + 1, j);
+      const float in_side = fetch(v, i, side ? j - 1 : j + 1);  // the inner neighbour
+      res[q] = 0.25f * ((up + dn) + (nbv[q] + in_side));
+    }
+    v.out[i * v.pitch + j] = res[q];
+  }
+  float* pub = v.col_out[side];
+  if (pub) {
+    if (i0 + 4 <= v.rows) {
+      *reinterpret_cast<float4*>(pub + i0) = make_float4(res[0], res[1], res[2], res[3]);
+    } else {
+      for (int q = 0; i0 + q < v.rows; ++q) pub[i0 + q] = res[q];
     }
   }
-  const bool edge_r0 = tr == 0, edge_r1 = tr == tiles_r - 1;
-  const bool edge_c0 = tc == 0, edge_c1 = tc == tiles_c - 1;
-  const bool interior = !(edge_r0 || edge_r1 || edge_c0 || edge_c1);
+}
+
+template <int TR>
+__global__ void __launch_bounds__(kThreads, 5)
+k_jacobi(const __grid_constant__ pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_interior) {
+  // column-strip CTAs first (few; they spin on the left / right flags at most while the
+  // tiles stream, so the sweep has no serial tail), interior tiles next, edge tiles
+  // last (index order = launch order)
+  const int per = (int)((v.rows + kStripRowsPerCta - 1) / kStripRowsPerCta);
+  const int nstrip = (v.nbr[2] ? per : 0) + (v.nbr[3] ? per : 0);
+  const int b = PM_STRIPS_FIRST ? ((int)blockIdx.x - nstrip + (int)gridDim.x) % (int)gridDim.x
+                                : (int)blockIdx.x;
+  const int ntiles = tiles_r * tiles_c;
   const bool has_nbr = v.nbr[0] || v.nbr[1] || v.nbr[2] || v.nbr[3];
-  if (has_nbr && b == 0 && threadIdx.x == 0 && sweep > 0) {
+  if (has_nbr && blockIdx.x == 0 && threadIdx.x == 0 && sweep > 0) {
     // every CTA of sweep - 1 has finished: tell the neighbours
     __threadfence_system();
     for (int d = 0; d < 4; ++d)
       if (v.nbr[d]) st_release_sys(v.nbr_flag_slot[d], sweep);
   }
-  if (!interior && has_nbr) {
-    // RAW: edge tiles read neighbour cells produced by their sweep - 1
-    if (threadIdx.x == 0) {
-      const bool need[4] = {edge_r0, edge_r1, edge_c0, edge_c1};
-      for (int d = 0; d < 4; ++d)
-        if (v.nbr[d] && need[d]) wait_flag(v.my_flags + v.nbr_rank[d], sweep);
+  if (b >= ntiles) {
+    const int k = b - ntiles;
+    const int side = (v.nbr[2] && k < per) ? 0 : 1;
+    column_strip(v, sweep, side, (v.nbr[2] && k < per) ? k : k - (v.nbr[2] ? per : 0));
+    return;
+  }
+  // middle tile rows in row-major order (the first / last tile column included: they
+  // wait for nothing, and a tail of edge-column tiles alone hits few DRAM channels --
+  // their segments are a power-of-two pitch apart), then the first and last tile rows
+  // (which wait for the up / down neighbours)
+  int tr, tc;
+  if (b < n_interior) {  // n_interior = (tiles_r - 2) * tiles_c
+    tr = 1 + b / tiles_c;
+    tc = b % tiles_c;
+  } else {
+    const int e = b - n_interior;
+    tr = e < tiles_c ? 0 : tiles_r - 1;
+    tc = e < tiles_c ? e : e - tiles_c;
+  }
+  const bool edge_r0 = tr == 0, edge_r1 = tr == tiles_r - 1;
+  const bool edge_c0 = tc == 0, edge_c1 = tc == tiles_c - 1;
+  const bool interior = !(edge_r0 || edge_r1 || edge_c0 || edge_c1);
+  if ((edge_r0 && v.nbr[0]) || (edge_r1 && v.nbr[1])) {
+    // RAW: the first / last row tiles read the up / down neighbour's rows of sweep - 1
+    // (the left / right columns are the strip CTAs')
+    if (threadIdx.x == 0 && sweep > 0) {
+      if (edge_r0 && v.nbr[0]) wait_flag(v.my_flags + v.nbr_rank[0], sweep);
+      if (edge_r1 && v.nbr[1]) wait_flag(v.my_flags + v.nbr_rank[1], sweep);
     }
     __syncthreads();
   }
+  // cells of a column a strip CTA computes (left / right neighbour present)
+  const bool skip_x = v.nbr[2] != nullptr, skip_w = v.nbr[3] != nullptr;
 
   const int64_t r0 = (int64_t)tr * TR;
   const int64_t c = (int64_t)tc * TC + threadIdx.x * 4;
@@ -130,11 +199,9 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
     float* __restrict__ po = v.out + r0 * v.pitch + c;
     const int64_t pitch = v.pitch;
     const bool left_edge = !interior && c == 0, right_edge = !interior && c + 4 == v.cols;
-    const float* pl = left_edge && v.nbr[2]
-                          ? v.nbr[2] + r0 * v.nbr_pitch[2] + (v.nbr_cols[2] - 1) : nullptr;
-    const float* pr = right_edge && v.nbr[3] ? v.nbr[3] + r0 * v.nbr_pitch[3] : nullptr;
     const bool g_first = left_edge && v.gcol0 == 0;
     const bool g_last = right_edge && v.gcol0 + v.cols == v.gcols;
+    const bool own_x = !(left_edge && skip_x), own_w = !(right_edge && skip_w);
     float4 up = __ldg(reinterpret_cast<const float4*>(p));
     float4 mid = __ldg(reinterpret_cast<const float4*>(p + pitch));
     for (int r8 = 0; r8 < TR; r8 += 8) {
@@ -144,10 +211,8 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
       for (int u = 0; u < 8; ++u) {
         const float* row = p + (int64_t)(r8 + u + 1) * pitch;
         dn[u] = __ldg(reinterpret_cast<const float4*>(row + pitch));
-        lf[u] = left_edge ? (pl ? ld_peer(pl + (int64_t)(r8 + u) * v.nbr_pitch[2]) : 0.f)
-                          : __ldg(row - 1);
-        rt[u] = right_edge ? (pr ? ld_peer(pr + (int64_t)(r8 + u) * v.nbr_pitch[3]) : 0.f)
-                           : __ldg(row + 4);
+        lf[u] = left_edge ? 0.f : __ldg(row - 1);
+        rt[u] = right_edge ? 0.f : __ldg(row + 4);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -158,7 +223,15 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
         o.w = 0.25f * ((up.w + dn[u].w) + (mid.z + rt[u]));
         if (g_first) o.x = mid.x;  // Dirichlet columns
         if (g_last) o.w = mid.w;
-        __stcs(reinterpret_cast<float4*>(po + (int64_t)(r8 + u) * pitch), o);
+        float* dst = po + (int64_t)(r8 + u) * pitch;
+        if (own_x && own_w) {
+          __stcs(reinterpret_cast<float4*>(dst), o);
+        } else {  // the strip CTA writes the neighbour-facing cell
+          if (own_x) dst[0] = o.x;
+          dst[1] = o.y;
+          dst[2] = o.z;
+          if (own_w) dst[3] = o.w;
+        }
         up = mid;
         mid = dn[u];
       }
@@ -172,8 +245,9 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
       if (i < 0 && v.nbr[0]) q = v.nbr[0] + (v.nbr_rows[0] - 1) * v.nbr_pitch[0] + c;
       if (i >= v.rows && v.nbr[1]) q = v.nbr[1] + c;
       if (!q) return make_float4(0.f, 0.f, 0.f, 0.f);  // global boundary: unused
-      return make_float4(ld_peer(q), ld_peer(q + 1), ld_peer(q + 2), ld_peer(q + 3));
+      return ld_peer4(q);  // 16-byte aligned: pitch % 4 == 0 on every GPU, c % 4 == 0
     };
+    const bool own_x = !(c == 0 && skip_x), own_w = !(c + 4 == v.cols && skip_w);
     const int64_t r1 = min(r0 + TR, v.rows);
     float4 up = row4(r0 - 1), mid = row4(r0);
     const bool g_first = v.gcol0 + c == 0, g_last = v.gcol0 + c + 3 == v.gcols - 1;
@@ -190,9 +264,7 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
         if (i >= r1) continue;
         dn[u] = row4(i + 1);
         if (c > 0) lf[u] = __ldg(v.in + i * v.pitch + c - 1);
-        else if (v.nbr[2]) lf[u] = ld_peer(v.nbr[2] + i * v.nbr_pitch[2] + (v.nbr_cols[2] - 1));
         if (c + 4 < v.cols) rt[u] = __ldg(v.in + i * v.pitch + c + 4);
-        else if (v.nbr[3]) rt[u] = ld_peer(v.nbr[3] + i * v.nbr_pitch[3]);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -210,7 +282,15 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
           if (g_first) o.x = mid.x;  // Dirichlet columns
           if (g_last) o.w = mid.w;
         }
-        __stcs(reinterpret_cast<float4*>(v.out + i * v.pitch + c), o);
+        float* dst = v.out + i * v.pitch + c;
+        if (own_x && own_w) {
+          __stcs(reinterpret_cast<float4*>(dst), o);
+        } else {  // the strip CTA writes the neighbour-facing cell
+          if (own_x) dst[0] = o.x;
+          dst[1] = o.y;
+          dst[2] = o.z;
+          if (own_w) dst[3] = o.w;
+        }
         up = mid;
         mid = dn[u];
       }
@@ -225,6 +305,10 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
       for (int q = 0; q < 4; ++q) {
         const int64_t j = c + q;
         if (j >= v.cols) { res[q] = 0.f; continue; }
+        if ((j == 0 && skip_x) || (j == v.cols - 1 && skip_w)) {  // a strip CTA's cell
+          res[q] = __int_as_float(0x7fc00000);
+          continue;
+        }
         const int64_t gj = v.gcol0 + j;
         if (gi == 0 || gj == 0 || gi == v.grows - 1 || gj == v.gcols - 1) {
           res[q] = __ldg(v.in + i * v.pitch + j);  // Dirichlet boundary
@@ -235,10 +319,12 @@ k_jacobi(const pm_stencil_view v, int sweep, int tiles_r, int tiles_c, int n_int
         }
       }
       float* o = v.out + i * v.pitch + c;
-      if (vec) {
+      const bool strip_cell = (c == 0 && skip_x) || (c + 4 >= v.cols && skip_w);
+      if (vec && !strip_cell) {
         *reinterpret_cast<float4*>(o) = make_float4(res[0], res[1], res[2], res[3]);
       } else {
-        for (int q = 0; q < 4 && c + q < v.cols; ++q) o[q] = res[q];
+        for (int q = 0; q < 4 && c + q < v.cols; ++q)
+          if (!((c + q == 0 && skip_x) || (c + q == v.cols - 1 && skip_w))) o[q] = res[q];
       }
     }
   }
@@ -257,8 +343,14 @@ extern "C" int pm_stencil_sweep(const pm_stencil_view* v, int32_t sweep, void* s
   const int TR = (tr_env == 32 || tr_env == 64 || tr_env == 128) ? tr_env : 16;
   const int tiles_r = (int)((v->rows + TR - 1) / TR);
   const int tiles_c = (int)((v->cols + pm::TC - 1) / pm::TC);
-  const int n_interior = std::max(tiles_r - 2, 0) * std::max(tiles_c - 2, 0);
-  const int total = tiles_r * tiles_c;
+  const int n_interior = std::max(tiles_r - 2, 0) * tiles_c;
+  const int per = (int)((v->rows + pm::kStripRowsPerCta - 1) / pm::kStripRowsPerCta);
+  if ((v->nbr[2] && !v->nbr_col[0]) || (v->nbr[3] && !v->nbr_col[1]) ||
+      (((uintptr_t)v->nbr_col[0] | (uintptr_t)v->nbr_col[1] | (uintptr_t)v->col_out[0] |
+        (uintptr_t)v->col_out[1]) & 15))
+    return pm::set_error("pm_stencil_sweep: left / right neighbours need 16-byte aligned "
+                         "column strips"), PM_ERR_INVALID;
+  const int total = tiles_r * tiles_c + (v->nbr[2] ? per : 0) + (v->nbr[3] ? per : 0);
   cudaStream_t s = (cudaStream_t)stream;
   switch (TR) {
     case 16: pm::k_jacobi<16><<<total, pm::kThreads, 0, s>>>(*v, sweep, tiles_r, tiles_c, n_interior); break;

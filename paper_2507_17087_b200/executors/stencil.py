@@ -46,7 +46,8 @@ class PmStencilView(ctypes.Structure):
                 ("nbr", ctypes.c_void_p * 4), ("nbr_pitch", ctypes.c_int64 * 4),
                 ("nbr_rows", ctypes.c_int64 * 4), ("nbr_cols", ctypes.c_int64 * 4),
                 ("my_flags", ctypes.c_void_p), ("nbr_flag_slot", ctypes.c_void_p * 4),
-                ("nbr_rank", ctypes.c_int32 * 4), ("ticket", ctypes.c_void_p)]
+                ("nbr_rank", ctypes.c_int32 * 4), ("ticket", ctypes.c_void_p),
+                ("col_out", ctypes.c_void_p * 2), ("nbr_col", ctypes.c_void_p * 2)]
 
 
 def stencil_mapper(world: int, mapping: str):
@@ -146,9 +147,17 @@ class MappedStencil:
         self.buf = [torch.zeros(self.mr, self.pitch, dtype=torch.float32, device=self.device)
                     for _ in range(3)]
         self.buf[0][:, :self.mc] = init_grid((r0, r1), (c0, c1), cols, seed, self.device)
+        # column strips per buffer: [0] my first column, [1] my last column, contiguous
+        # (the left / right neighbours read them with 16-byte NVLink loads)
+        rp = (self.mr + 3) // 4 * 4
+        self.strips = [torch.zeros(2, rp, dtype=torch.float32, device=self.device)
+                       for _ in range(3)]
+        self.strips[0][0, :self.mr] = self.buf[0][:, 0]
+        self.strips[0][1, :self.mr] = self.buf[0][:, self.mc - 1]
         self.flags = torch.zeros(max(world, 1), dtype=torch.int32, device=self.device)
         self.ticket = torch.zeros(1, dtype=torch.int32, device=self.device)
         names = {f"b{i}": b for i, b in enumerate(self.buf)}
+        names.update({f"s{i}": t for i, t in enumerate(self.strips)})
         names["flags"] = self.flags
         self.peers = PeerBuffers(names, rank, world, group)
         self.nbrs = block_neighbors(self.rects, rank, rows, cols)
@@ -169,6 +178,13 @@ class MappedStencil:
         v.grow0, v.gcol0, v.grows, v.gcols = r0, c0, self.rows, self.cols
         v.my_flags = self.flags.data_ptr()
         v.ticket = self.ticket.data_ptr()
+        out_strip = self.strips[(s + 1) % 3]
+        v.col_out[0], v.col_out[1] = out_strip[0].data_ptr(), out_strip[1].data_ptr()
+        rp4 = 4 * self.strips[0].shape[1]  # bytes per strip row of the 2 x rp tensor
+        for side, d in ((0, 2), (1, 3)):  # the left neighbour's last / right's first column
+            q = self.nbrs[d]
+            v.nbr_col[side] = None if q is None else \
+                self.peers.ptrs[f"s{s % 3}"][q] + (rp4 if side == 0 else 0)
         for d, q in enumerate(self.nbrs):
             if q is None:
                 v.nbr[d] = None
