@@ -177,6 +177,10 @@ struct Params {
                       // draw ticket_end - 1 is the last and zeroes the counter
   int k_split;        // 1-SM kernel: K slices per output tile (<= 1: none); > 1 adds
                       // every slice's partial product into C with vector red.add
+  int wave_sync;      // wide kernel: a tile of wave w (= ticket / pairs) starts loading
+                      // only once every tile of wave w - 1 has issued its last load
+                      // (tile_counter[1] counts them): the co-resident tiles then walk K
+                      // in step and share their A / B panels in L2
 };
 
 __device__ __forceinline__ void tile_coords(int t, const Params& p, int& tm, int& tn) {
@@ -914,6 +918,12 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
         coords(t, tm, tn);
         const int am = tm * WM + crank * 128;
         const int bn = tn * WN + crank * 128;
+        if (p.wave_sync && leader) {
+          // wave barrier: every tile of the previous wave has issued its last load
+          const int need = (t / npairs) * npairs;
+          volatile int* done = p.tile_counter + 1;
+          while (*done < need) __nanosleep(128);
+        }
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = full0 + stage * 8;
@@ -928,6 +938,7 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
           tma_load_2sm(&map_b, fb, sb + stage * BW_BYTES, kb * BK, bn);
           if (++stage == kStagesW) { stage = 0; phase ^= 1; }
         }
+        if (p.wave_sync && leader) atomicAdd(p.tile_counter + 1, 1);
       }
     }
   } else if (warp == 1) {
@@ -1273,7 +1284,8 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
       rc = tile_ticket(dev, stream, &p.tile_counter);
       if (rc) return rc;
       p.ticket_end = (int)(pairs_needed + pairs);
-      PM_CUDA_TRY(cudaMemsetAsync(p.tile_counter, 0, sizeof(int), (cudaStream_t)stream));
+      p.wave_sync = getenv("PM_GEMM_WAVESYNC") ? atoi(getenv("PM_GEMM_WAVESYNC")) : 0;
+      PM_CUDA_TRY(cudaMemsetAsync(p.tile_counter, 0, 2 * sizeof(int), (cudaStream_t)stream));
       wide::k_gemm_bf16_wide<<<(unsigned)(2 * pairs), wide::kThreadsW, wide::SMEMW,
                                (cudaStream_t)stream>>>(ma, mb, mc, p);
     } else {
