@@ -17,9 +17,10 @@ GPU (a, b, c) computes the partial product A[a, c] * B[c, b] over K block c:
     epilogue reduce-adds the tile straight into the owner's C buffer over
     NVLink (TMA `cp.reduce.async.bulk.tensor .add` on an IPC-mapped pointer) --
     the collective is fused into the GEMM, there is no separate NCCL call.
-C is double-buffered; one stream-ordered barrier per step (through peer memory,
-csrc/barrier.cu -- no NCCL) separates the zeroing of a buffer from the peers'
-adds into it.
+The launch for this GPU's own rows goes first and overwrites them (plain TMA
+stores: C is never zeroed, never read back); one stream-ordered barrier per step
+(through peer memory, csrc/barrier.cu -- no NCCL) then lets the peers' launches
+reduce-add into them.  C is double-buffered.
 """
 
 from __future__ import annotations
@@ -129,8 +130,11 @@ class MappedGemm3D:
             r = split(mb, pn, b2)
             self.pulls.append(("A", self.owner[(a, b2, c)], r, si % 4, torch.cuda.Event()))
             si += 1
-        # one GEMM per destination in the k-group; the local destination last
-        order = [(c + 1 + i) % pk for i in range(pk)]
+        # one GEMM per destination in the k-group: the local destination first, written
+        # with plain (TMA) stores -- it initialises this GPU's rows of C, so C is never
+        # zeroed nor read back -- then, after a barrier, the peers' rows with TMA
+        # reduce-adds over NVLink
+        order = [(c + i) % pk for i in range(pk)]
         self.gemms = [(split(mb, pk, d), self.owner[(a, b, d)]) for d in order]
         self.done = torch.cuda.Event()
         self.done.record()
@@ -160,14 +164,10 @@ class MappedGemm3D:
         cs = stream or torch.cuda.current_stream()
         buf = self.step_i % 2
         self.step_i += 1
-        if self.reduce:
-            # C[buf] was last added into two steps ago; every GPU finished those GEMMs
-            # before it joined the previous step's barrier, which we passed: zero it now,
-            # and only then (barrier) may the peers add into it.  C[1-buf] -- the previous
-            # step's result -- stays intact during this step.
-            with torch.cuda.stream(cs):  # ordered with the GEMMs on cs
-                self.C[buf].zero_()
-            self._barrier(cs)
+        # C[buf] was last added into by the peers two steps ago, before each of them
+        # joined the previous step's barrier, which we passed: the local GEMM may
+        # overwrite it now; the peers add into it only after this step's barrier.
+        # C[1-buf] -- the previous step's result -- stays intact during this step.
         for s in self.streams:
             s.wait_event(self.done)
         for name, q, (r0, r1), si, ev in self.pulls:
@@ -180,11 +180,13 @@ class MappedGemm3D:
         for _, _, _, _, ev in self.pulls:
             cs.wait_event(ev)
         lib = native.lib()
-        for (r0, r1), dst in self.gemms:
+        for i, ((r0, r1), dst) in enumerate(self.gemms):
+            if i == 1:
+                self._barrier(cs)  # every GPU has written its own rows of C[buf]
             cptr = self.peers.ptrs[f"C{buf}"][dst]
             native.check(lib.pm_gemm_bf16(
                 self.A[r0:r1].data_ptr(), self.kb, self.Bt.data_ptr(), self.kb, cptr, self.nb,
-                r1 - r0, self.nb, self.kb, 0, 2 if self.reduce else 0, native.stream_ptr(cs)),
+                r1 - r0, self.nb, self.kb, 0, 2 if i else 0, native.stream_ptr(cs)),
                 "pm_gemm_bf16")
         self.done.record(cs)
         return self.C[buf]
