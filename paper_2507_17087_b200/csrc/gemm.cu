@@ -819,7 +819,7 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
   uint64_t* full = bars;                    // leader's (count 2)
   uint64_t* empty = bars + kStagesW;        // per CTA (leader's commit)
   uint64_t* tfull = bars + 2 * kStagesW;    // per CTA (leader's commit)
-  uint64_t* tempty = bars + 2 * kStagesW + 1;  // [2] leader's, count 8 each
+  uint64_t* tempty = bars + 2 * kStagesW + 1;  // [2] leader's, count 16 each
   uint64_t* qfull = bars + 2 * kStagesW + 3;   // [kQ] per CTA: tile index published
   uint64_t* qempty = qfull + kQ;               // [kQ] leader's: all consumers read it
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(qempty + kQ);
@@ -845,8 +845,8 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
       mbar_init(&empty[s], 1);
     }
     mbar_init(&tfull[0], 1);
-    mbar_init(&tempty[0], 8);
-    mbar_init(&tempty[1], 8);
+    mbar_init(&tempty[0], 16);  // 8 epilogue warps x 2 CTAs per TMEM half
+    mbar_init(&tempty[1], 16);
     for (int i = 0; i < kQ; ++i) {
       mbar_init(&qfull[i], 1);
       mbar_init(&qempty[i], kQConsumers);
@@ -982,9 +982,12 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
       }
     }
   } else if (warp >= 4) {
-    const int h = (warp - 4) >> 2;  // TMEM half drained by this warp
+    // all 8 epilogue warps drain TMEM half 0 first, then half 1 (warp j of a lane
+    // quarter takes column chunks 4j .. 4j + 3 of each half): half 0 is free for the
+    // next tile's MMAs after half of the drain time
+    const int j = (warp - 4) >> 2;  // column half of each TMEM half drained by this warp
     const int q = warp & 3;         // TMEM lane quarter this warp may access
-    const uint32_t tempty_h = mapa_shared(smem_u32(&tempty[h]), 0);
+    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
     for (int it = 0;; ++it) {
       int t = 0;
       if (lane == 0) t = next_tile();
@@ -994,23 +997,26 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
       coords(t, tm, tn);
       mbar_wait(&tfull[0], it & 1);
       tc_fence_after();
-      const int row0 = tm * WM + h * 256 + crank * 128 + q * 32;
       uint8_t* buf = epi + (warp - 4) * EPI_BUF;
 #pragma unroll 1
-      for (int ch = 0; ch < WN / 32; ++ch) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + h * WN + ch * 32, v);
-        if (p.tma_store) {
-          if (!p.debug_nostore)
-            store_chunk_tma(&map_c, p.c32 != nullptr, p.accumulate != 0, buf, lane, row0,
-                            tn * WN + ch * 32, v);
-        } else {
-          store_chunk(p, row0 + lane, tn * WN + ch * 32, v);
+      for (int h = 0; h < 2; ++h) {
+        const int row0 = tm * WM + h * 256 + crank * 128 + q * 32;
+#pragma unroll 1
+        for (int ch = 4 * j; ch < 4 * j + WN / 64; ++ch) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + h * WN + ch * 32, v);
+          if (p.tma_store) {
+            if (!p.debug_nostore)
+              store_chunk_tma(&map_c, p.c32 != nullptr, p.accumulate != 0, buf, lane, row0,
+                              tn * WN + ch * 32, v);
+          } else {
+            store_chunk(p, row0 + lane, tn * WN + ch * 32, v);
+          }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty0 + 8 * h);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_h);
     }
     if (lane == 0) {
       // the TMA stores / reduce-adds (async proxy, possibly into a peer GPU's C) have
