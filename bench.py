@@ -197,7 +197,7 @@ def run_mapping(args, rank, world, local, mapping, mnk=None):
     launch_ms = []
     for _ in range(max(2, min(args.steps, 5))):
         evs = []
-        orig = ex.step
+        orig = ex.step_python  # op by op, so each tile_gemm launch can be bracketed
 
         from paper_2507_17087_b200 import gemm as G
 

@@ -330,6 +330,49 @@ typedef struct pm_circuit_view {
 } pm_circuit_view;
 int pm_circuit_step(const pm_circuit_view* view, int32_t phase, void* stream);
 
+/* Step programs: a mapped executor's per-step schedule as data, replayed by one
+ * call (the C-ABI form of the executors, SURVEY §8(b) pm_run_*: the planners --
+ * executors/summa.py plan_panels, grid3d.py, cannon.py cannon_schedule -- build
+ * the op list once over fixed device / peer pointers; any host can build one).
+ *   PM_STEP_PULL          pitched copy-engine copy dst <- src (dpitch / spitch /
+ *                         width bytes x height rows, peer or local) on copy lane
+ *                         `lane` (0..PM_STEP_LANES-1), or on the compute stream
+ *                         when lane == -1;
+ *   PM_STEP_WAIT          the compute stream waits for the lane pull at op index
+ *                         `lane` (an earlier PM_STEP_PULL with lane >= 0);
+ *   PM_STEP_GEMM_BF16     pm_gemm_bf16(src = A, lda, b = Bt, ldb, dst = C, ldc, m, n,
+ *                         k, c_bf16, accumulate) on the compute stream;
+ *   PM_STEP_GEMM_TF32     pm_gemm_tf32(src, lda, b, ldb, dst, ldc, m, n, k, accumulate);
+ *   PM_STEP_MEMSET        zero `width` bytes at dst (compute stream);
+ *   PM_STEP_BARRIER       pm_peer_barrier(barrier);
+ *   PM_STEP_COPY_BARRIER  pm_peer_copy_barrier(barrier, copies, n_copies, ticket).
+ * pm_steps_run: the lanes fork from `stream` at the first lane pull (after
+ * everything already queued on it) and join back at the end of the step; no
+ * host synchronisation; capturable in a CUDA graph.  The program keeps its own
+ * copy of the ops (and copy lists) but not of the memory they point to. */
+#define PM_STEP_LANES 4
+enum {
+  PM_STEP_PULL = 0, PM_STEP_WAIT = 1, PM_STEP_GEMM_BF16 = 2, PM_STEP_GEMM_TF32 = 3,
+  PM_STEP_MEMSET = 4, PM_STEP_BARRIER = 5, PM_STEP_COPY_BARRIER = 6
+};
+typedef struct pm_step_op {
+  int32_t kind, lane;
+  void* dst;
+  const void* src;
+  const void* b;
+  int64_t dpitch, spitch, width, height;
+  int64_t lda, ldb, ldc, m, n, k;
+  int32_t c_bf16, accumulate;
+  const void* barrier;            /* pm_peer_barrier_view*                     */
+  const pm_peer_copy* copies;
+  int32_t n_copies;
+  uint32_t* ticket;
+} pm_step_op;
+typedef struct pm_steps pm_steps;
+int pm_steps_create(const pm_step_op* ops, int32_t n, pm_steps** out);
+int pm_steps_run(pm_steps* program, void* stream);
+void pm_steps_destroy(pm_steps* program);
+
 /* One phase of a PENNANT-style Lagrangian hydro step (the paper's PENNANT
  * workload, after Ferenbaugh 2015; no reference code, parity
  * against oracle/hydro.py).  Quadrilateral zones with counter-clockwise point

@@ -208,29 +208,39 @@ class MappedCannon:
         return self.C[buf]
 
     def _issue(self, buf, cs):
-        torch = native.require_cuda()
-        lib = native.lib()
+        """One multiply into C[buf]: its step program (built once per buffer) run on cs."""
+        progs = self.__dict__.setdefault("_programs", {})
+        if buf not in progs:
+            progs[buf] = self._build(buf)
+        progs[buf].run(cs)
+
+    def _build(self, buf):
+        """The schedule (cannon_schedule) of one multiply into C[buf] as a StepProgram
+        (csrc/steps.cpp): SM-copy + barrier launches for small blocks, copy-engine
+        pulls + barriers for large ones, TF32 / bf16 GEMMs reduce-added into the
+        owning layer."""
+        from ..peer import StepProgram
+
+        prog = StepProgram()
         q, c = self.q, self.c
         i, j, l = self.coord
         if c > 1:
             # the layers' adds into C[buf] date from two steps ago and all finished before
             # the previous step's barriers; the schedule's first barrier orders this zeroing
             # before any peer adds into it again
-            with torch.cuda.stream(cs):
-                self.C[buf].zero_()
+            prog.memset(self.C[buf].data_ptr(), self.C[buf].numel() * 4)
         moved = 0
         first = True  # the first local product overwrites C (Cannon); 2.5D always adds
         pending = []  # a round's pulls, issued with its closing barrier (one launch)
         for op in cannon_schedule(q, c, self.coord):
             if op[0] == "barrier":
                 if self._bar is not None and pending and self._fused_pulls:
-                    self._bar.copy_then_wait([(d, sp, w * h) for d, sp, w, h in pending], cs)
+                    prog.copy_barrier(self._bar, [(d, sp, w * h) for d, sp, w, h in pending])
                 else:
-                    from ..peer import copy2d
-
-                    for d, sp, w, h in pending:  # copy engines, pitched rows
-                        copy2d(d, w, sp, w, w, h, cs)
-                    self._barrier(cs)
+                    for d, sp, w, h in pending:  # copy engines, pitched rows, in order
+                        prog.pull(d, w, sp, w, w, h, lane=-1)
+                    if self._bar is not None:
+                        prog.barrier(self._bar)
                 pending = []
             elif op[0] == "pull":
                 _, name, src, (kind, slot) = op
@@ -248,18 +258,14 @@ class MappedCannon:
                 a = a_blk[r0:r1]
                 acc = 2 if c > 1 else int(not first)
                 if self.dtype == "fp32":
-                    native.check(lib.pm_gemm_tf32(a.data_ptr(), self.nb, b_blk.data_ptr(),
-                                                  self.nb, cptr, self.nb, r1 - r0, self.nb,
-                                                  self.nb, acc, native.stream_ptr(cs)),
-                                 "pm_gemm_tf32")
+                    prog.gemm_tf32(a.data_ptr(), self.nb, b_blk.data_ptr(), self.nb, cptr,
+                                   self.nb, r1 - r0, self.nb, self.nb, acc)
                 else:
-                    native.check(lib.pm_gemm_bf16(a.data_ptr(), self.nb, b_blk.data_ptr(),
-                                                  self.nb, cptr, self.nb, r1 - r0, self.nb,
-                                                  self.nb, 0, acc, native.stream_ptr(cs)),
-                                 "pm_gemm_bf16")
+                    prog.gemm_bf16(a.data_ptr(), self.nb, b_blk.data_ptr(), self.nb, cptr,
+                                   self.nb, r1 - r0, self.nb, self.nb, 0, acc)
                 first = False
         self.moved_blocks = moved
-        _ = torch
+        return prog.build()
 
     def result(self):
         self._barrier()
@@ -271,6 +277,8 @@ class MappedCannon:
         if self._graphs:
             native.require_cuda().cuda.synchronize()
             self._graphs.clear()
+        for prog in self.__dict__.get("_programs", {}).values():
+            prog.close()
         if self._bar is not None:
             self._bar.close()
         self.peers.close()

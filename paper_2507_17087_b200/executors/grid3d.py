@@ -157,10 +157,37 @@ class MappedGemm3D:
         if self._bar is not None:  # stream-ordered: runs after the queued GEMMs
             self._bar(stream)
 
+    def _program(self, buf):
+        """One step into C[buf] as a StepProgram (csrc/steps.cpp): the all-gather pulls
+        on copy lanes, the compute stream waiting for them, the local-rows GEMM
+        (plain stores), a barrier, the peers' rows (TMA reduce-adds over NVLink)."""
+        from ..peer import StepProgram
+
+        progs = self.__dict__.setdefault("_programs", {})
+        if buf in progs:
+            return progs[buf]
+        prog = StepProgram()
+        at = []
+        for name, q, (r0, r1), si, _ev in self.pulls:
+            t = self.A if name == "A" else self.Bt
+            pitch = t.shape[1] * 2
+            off = r0 * pitch
+            at.append(prog.pull(self.peers.ptrs[name][self.rank] + off, pitch,
+                                self.peers.ptrs[name][q] + off, pitch, pitch, r1 - r0,
+                                lane=si % 4))
+        for i in at:
+            prog.wait(i)
+        for i, ((r0, r1), dst) in enumerate(self.gemms):
+            if i == 1 and self._bar is not None:
+                prog.barrier(self._bar)  # every GPU has written its own rows of C[buf]
+            prog.gemm_bf16(self.A[r0:r1].data_ptr(), self.kb, self.Bt.data_ptr(), self.kb,
+                           self.peers.ptrs[f"C{buf}"][dst], self.nb, r1 - r0, self.nb, self.kb,
+                           0, 2 if i else 0)
+        progs[buf] = prog.build()
+        return progs[buf]
+
     def step(self, stream=None):
         torch = native.require_cuda()
-        from ..peer import copy2d
-
         cs = stream or torch.cuda.current_stream()
         buf = self.step_i % 2
         self.step_i += 1
@@ -168,26 +195,7 @@ class MappedGemm3D:
         # joined the previous step's barrier, which we passed: the local GEMM may
         # overwrite it now; the peers add into it only after this step's barrier.
         # C[1-buf] -- the previous step's result -- stays intact during this step.
-        for s in self.streams:
-            s.wait_event(self.done)
-        for name, q, (r0, r1), si, ev in self.pulls:
-            t = self.A if name == "A" else self.Bt
-            pitch = t.shape[1] * 2
-            off = r0 * pitch
-            copy2d(self.peers.ptrs[name][self.rank] + off, pitch, self.peers.ptrs[name][q] + off,
-                   pitch, pitch, r1 - r0, self.streams[si])
-            ev.record(self.streams[si])
-        for _, _, _, _, ev in self.pulls:
-            cs.wait_event(ev)
-        lib = native.lib()
-        for i, ((r0, r1), dst) in enumerate(self.gemms):
-            if i == 1:
-                self._barrier(cs)  # every GPU has written its own rows of C[buf]
-            cptr = self.peers.ptrs[f"C{buf}"][dst]
-            native.check(lib.pm_gemm_bf16(
-                self.A[r0:r1].data_ptr(), self.kb, self.Bt.data_ptr(), self.kb, cptr, self.nb,
-                r1 - r0, self.nb, self.kb, 0, 2 if i else 0, native.stream_ptr(cs)),
-                "pm_gemm_bf16")
+        self._program(buf).run(cs)
         self.done.record(cs)
         return self.C[buf]
 
@@ -198,6 +206,8 @@ class MappedGemm3D:
         return self.C[(self.step_i - 1) % 2]
 
     def close(self):
+        for prog in self.__dict__.get("_programs", {}).values():
+            prog.close()
         if self._bar is not None:
             self._bar.close()
         self.peers.close()

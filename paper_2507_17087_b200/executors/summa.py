@@ -329,9 +329,53 @@ class MappedGemm:
         dst = self.peers.ptrs[name][self.rank] + (row0 * self.K + k0) * esz
         copy2d(dst, pitch, src, pitch, (k1 - k0) * esz, nrows, stream)
 
+    def _program(self):
+        """The step as a StepProgram (csrc/steps.cpp): the same pulls on the same copy
+        lanes, waits and GEMM launches as step_python, replayed by one C call.  Bound
+        to the current A / Bt / C tensors (cached per binding)."""
+        from ..peer import StepProgram
+
+        key = (self.A.data_ptr(), self.Bt.data_ptr(), self.C.data_ptr())
+        progs = self.__dict__.setdefault("_programs", {})
+        prog = progs.get(key)
+        if prog is not None:
+            return prog
+        prog = StepProgram()
+        esz, K = 2, self.K
+        pitch = K * esz
+        at = {}
+        for i, (name, q, row0, rows, k0, k1, si, _ev) in enumerate(self.pulls):
+            src = self.peers.ptrs[name][q] + (row0 * K + k0) * esz
+            dst = (self.A if name == "A" else self.Bt).data_ptr() + (row0 * K + k0) * esz
+            at[i] = prog.pull(dst, pitch, src, pitch, (k1 - k0) * esz, rows, lane=si % 4)
+        ev_index = {id(p[-1]): i for i, p in enumerate(self.pulls)}
+        c_bf16 = int(self.C.dtype != native.require_cuda().float32)
+        csz = self.C.element_size()
+        nc = self.C.shape[1]
+        for r0, r1, k0, k1, acc, evs in self.gemms:
+            for ev in evs:
+                prog.wait(at[ev_index[id(ev)]])
+            prog.gemm_bf16(self.A.data_ptr() + (r0 * K + k0) * esz, K,
+                           self.Bt.data_ptr() + k0 * esz, K, self.C.data_ptr() + r0 * nc * csz,
+                           nc, r1 - r0, nc, k1 - k0, c_bf16, int(acc))
+        progs[key] = prog.build()
+        return prog
+
     def step(self, stream=None, ready=None):
-        """One full multiply, stream-ordered (no host synchronisation).  `ready`: an
-        optional event the pulls also wait for (e.g. every GPU's operands landed)."""
+        """One full multiply, stream-ordered (no host synchronisation), as one
+        step-program call.  `ready`: an optional event the pulls also wait for (e.g.
+        every GPU's operands landed)."""
+        torch = native.require_cuda()
+        cs = stream or torch.cuda.current_stream()
+        if ready is not None:
+            cs.wait_event(ready)  # the lanes fork from cs after it
+        self._program().run(cs)
+        self.done.record(cs)
+        return self.C
+
+    def step_python(self, stream=None, ready=None):
+        """The same multiply issued op by op from Python (tile_gemm per launch, e.g.
+        for per-launch timing)."""
         torch = native.require_cuda()
         from ..gemm import tile_gemm
 
@@ -355,4 +399,6 @@ class MappedGemm:
         return self.C
 
     def close(self):
+        for prog in self.__dict__.get("_programs", {}).values():
+            prog.close()
         self.peers.close()

@@ -136,5 +136,8 @@ SIGNATURES["pm_map_scatter"] = (ctypes.c_int, [_VP, _VP, _I64, _I64, _I32, _VP, 
 SIGNATURES["pm_compile_check_probe"] = (ctypes.c_int, [ctypes.POINTER(PmProgram)])
 SIGNATURES["pm_plan_regs"] = (ctypes.c_int, [_VP])
 SIGNATURES["pm_map_probe"] = (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP])
+SIGNATURES["pm_steps_create"] = (ctypes.c_int, [_VP, _I32, ctypes.POINTER(_VP)])
+SIGNATURES["pm_steps_run"] = (ctypes.c_int, [_VP, _VP])
+SIGNATURES["pm_steps_destroy"] = (None, [_VP])
 SIGNATURES["pm_gemm_tf32"] = (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64,
                                              _I32, _VP])

@@ -112,3 +112,80 @@ def copy2d(dst: int, dpitch: int, src: int, spitch: int, width: int, height: int
     """Pitched byte copy on the copy engines (peer or local), stream-ordered."""
     native.check(native.lib().pm_copy2d_async(dst, dpitch, src, spitch, width, height,
                                               native.stream_ptr(stream)), "pm_copy2d_async")
+
+
+class PmStepOp(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("lane", ctypes.c_int32), ("dst", ctypes.c_void_p),
+                ("src", ctypes.c_void_p), ("b", ctypes.c_void_p), ("dpitch", ctypes.c_int64),
+                ("spitch", ctypes.c_int64), ("width", ctypes.c_int64), ("height", ctypes.c_int64),
+                ("lda", ctypes.c_int64), ("ldb", ctypes.c_int64), ("ldc", ctypes.c_int64),
+                ("m", ctypes.c_int64), ("n", ctypes.c_int64), ("k", ctypes.c_int64),
+                ("c_bf16", ctypes.c_int32), ("accumulate", ctypes.c_int32),
+                ("barrier", ctypes.c_void_p), ("copies", ctypes.c_void_p),
+                ("n_copies", ctypes.c_int32), ("ticket", ctypes.c_void_p)]
+
+
+PULL, WAIT, GEMM_BF16, GEMM_TF32, MEMSET, BARRIER, COPY_BARRIER = range(7)
+LANES = 4
+
+
+class StepProgram:
+    """One GPU's per-step schedule as data (csrc/steps.cpp, pm_steps_*): built once by
+    an executor's planner over fixed device / peer pointers, replayed by one C call
+    per step (`run`).  Ops: pull (copy-engine copy on a lane, or on the compute
+    stream with lane=-1), wait (the compute stream on a lane pull), GEMMs, memset,
+    peer barriers."""
+
+    def __init__(self):
+        self.ops = []
+        self._keep = []   # ctypes objects the ops point to (barrier views, copy lists)
+        self._handle = None
+
+    def pull(self, dst, dpitch, src, spitch, width, height, lane=0) -> int:
+        self.ops.append(PmStepOp(kind=PULL, lane=lane, dst=dst, src=src, dpitch=dpitch,
+                                 spitch=spitch, width=width, height=height))
+        return len(self.ops) - 1
+
+    def wait(self, pull_index: int) -> None:
+        self.ops.append(PmStepOp(kind=WAIT, lane=pull_index))
+
+    def gemm_bf16(self, A, lda, Bt, ldb, C, ldc, m, n, k, c_bf16=0, accumulate=0) -> None:
+        self.ops.append(PmStepOp(kind=GEMM_BF16, src=A, lda=lda, b=Bt, ldb=ldb, dst=C, ldc=ldc,
+                                 m=m, n=n, k=k, c_bf16=c_bf16, accumulate=accumulate))
+
+    def gemm_tf32(self, A, lda, Bt, ldb, C, ldc, m, n, k, accumulate=0) -> None:
+        self.ops.append(PmStepOp(kind=GEMM_TF32, src=A, lda=lda, b=Bt, ldb=ldb, dst=C, ldc=ldc,
+                                 m=m, n=n, k=k, accumulate=accumulate))
+
+    def memset(self, ptr, nbytes) -> None:
+        self.ops.append(PmStepOp(kind=MEMSET, dst=ptr, width=nbytes))
+
+    def barrier(self, bar: "PeerBarrier") -> None:
+        self._keep.append(bar.view)
+        self.ops.append(PmStepOp(kind=BARRIER, barrier=ctypes.addressof(bar.view)))
+
+    def copy_barrier(self, bar: "PeerBarrier", copies) -> None:
+        if len(copies) > 4:
+            raise ValueError("at most 4 copies per launch")
+        arr = (PmPeerCopy * max(1, len(copies)))(*[PmPeerCopy(d, s_, n) for d, s_, n in copies])
+        self._keep += [bar.view, arr]
+        self.ops.append(PmStepOp(kind=COPY_BARRIER, barrier=ctypes.addressof(bar.view),
+                                 copies=ctypes.addressof(arr), n_copies=len(copies),
+                                 ticket=bar.ticket.data_ptr()))
+
+    def build(self) -> "StepProgram":
+        arr = (PmStepOp * max(1, len(self.ops)))(*self.ops)
+        out = ctypes.c_void_p()
+        native.check(native.lib().pm_steps_create(arr, len(self.ops), ctypes.byref(out)),
+                     "pm_steps_create")
+        self._handle = out.value
+        return self
+
+    def run(self, stream=None) -> None:
+        native.check(native.lib().pm_steps_run(self._handle, native.stream_ptr(stream)),
+                     "pm_steps_run")
+
+    def close(self) -> None:
+        if self._handle:
+            native.lib().pm_steps_destroy(self._handle)
+            self._handle = None
