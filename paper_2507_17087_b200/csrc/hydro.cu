@@ -36,49 +36,33 @@ struct HydroArgs {
 __device__ __forceinline__ int rk(int ref) { return (int)((unsigned)ref >> 27); }
 __device__ __forceinline__ int sl(int ref) { return ref & ((1 << 27) - 1); }
 
-__global__ void __launch_bounds__(256)
-k_hydro_zones(const __grid_constant__ HydroArgs a) {
-  const pm_hydro_view& v = a.v;
-  const long long z = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nz = v.n_zones;
-  if (z >= nz) return;
-  int ref[4];
-  float x[4], y[4], u[4], w[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) ref[k] = __ldg(v.z2p + k * nz + z);
-  // point state is read-only during this phase (also on the peers): one 16-byte
-  // non-coherent load of (x, y, u, v) per corner
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int r = rk(ref[k]), s = sl(ref[k]);
-    const float4 q = __ldg(reinterpret_cast<const float4*>(v.pst[r]) + s);
-    x[k] = q.x;
-    y[k] = q.y;
-    u[k] = q.z;
-    w[k] = q.w;
-  }
+// one zone: area, PdV energy update, EOS, artificial viscosity, corner forces
+// deposited into the owners' force arrays (ref[k]: the zone's point references,
+// q[k]: their (x, y, u, v))
+__device__ __forceinline__ void hydro_zone(const pm_hydro_view& v, const int (&ref)[4],
+                                           const float4 (&st)[4], float zm, float ze, float za,
+                                           float zpe, float& e_out, float& a_out, float& pe_out) {
   float area = 0.f, dadt = 0.f;
   float nx[4], ny[4];  // edge k (point k -> k+1) outward normal scaled by its length
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int k1 = (k + 1) & 3;
-    area += x[k] * y[k1] - x[k1] * y[k];
-    nx[k] = y[k1] - y[k];
-    ny[k] = x[k] - x[k1];
-    dadt += (u[k] + u[k1]) * nx[k] + (w[k] + w[k1]) * ny[k];
+    area += st[k].x * st[k1].y - st[k1].x * st[k].y;
+    nx[k] = st[k1].y - st[k].y;
+    ny[k] = st[k].x - st[k1].x;
+    dadt += (st[k].z + st[k1].z) * nx[k] + (st[k].w + st[k1].w) * ny[k];
   }
   area *= 0.5f;
   dadt *= 0.5f;
-  const float zm = __ldg(v.zm + z);
   // PdV work of the last step's pressure over this step's volume change
-  const float e = v.ze[z] - v.zpe[z] * (area - v.za[z]) / zm;
+  const float e = ze - zpe * (area - za) / zm;
   const float rho = zm / area;
   const float p = (v.gamma - 1.0f) * rho * e;
   const float q = dadt < 0.f ? v.cq * rho * dadt * dadt / area : 0.f;
   const float pe = p + q;
-  v.ze[z] = e;
-  v.za[z] = area;
-  v.zpe[z] = pe;
+  e_out = e;
+  a_out = area;
+  pe_out = pe;
   // corner force of point k = half of each adjacent edge's pressure force, deposited
   // in the owner's memory: one 8-byte vector atomic (sm_90+ float2 atomicAdd) into
   // this GPU's points; two 4-byte float atomics -- the form NVLink peer atomics
@@ -95,6 +79,31 @@ k_hydro_zones(const __grid_constant__ HydroArgs a) {
       atomicAdd(v.fxy[r] + 2 * s + 1, fy);
     }
   }
+}
+
+__device__ __forceinline__ float4 point_state(const pm_hydro_view& v, int ref) {
+  // point state is read-only during this phase (also on the peers): one 16-byte
+  // non-coherent load of (x, y, u, v)
+  return __ldg(reinterpret_cast<const float4*>(v.pst[rk(ref)]) + sl(ref));
+}
+
+__global__ void __launch_bounds__(256)
+k_hydro_zones(const __grid_constant__ HydroArgs a) {
+  const pm_hydro_view& v = a.v;
+  const long long z = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nz = v.n_zones;
+  if (z >= nz) return;
+  int ref[4];
+  float4 st[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) ref[k] = __ldg(v.z2p + k * nz + z);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) st[k] = point_state(v, ref[k]);
+  float e, ar, pe;
+  hydro_zone(v, ref, st, __ldg(v.zm + z), v.ze[z], v.za[z], v.zpe[z], e, ar, pe);
+  v.ze[z] = e;
+  v.za[z] = ar;
+  v.zpe[z] = pe;
 }
 
 __device__ __forceinline__ float4 hydro_move(float4 q, float2 f, float m, int bc, float dt) {
@@ -147,6 +156,8 @@ int pm_hydro_step(const pm_hydro_view* view, int32_t phase, void* stream) {
   pm::HydroArgs a{*view};
   if (phase == 0) {
     if (view->n_zones == 0) return PM_OK;
+    // one zone per thread (two per thread, with vector zone loads and eight gathers in
+    // flight, was slower: 1.21 vs 0.96 ms at 67M zones)
     pm::k_hydro_zones<<<(unsigned)((view->n_zones + 255) / 256), 256, 0, s>>>(a);
   } else if (phase == 1) {
     if (view->n_points == 0) return PM_OK;
