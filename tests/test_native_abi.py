@@ -103,3 +103,45 @@ def test_device_entry_points_fail_loudly_without_gpu():
                         MachineShape("GPU", 1, 1))
     with pytest.raises(native.NativeError):
         fn.map_ispace((4,))
+
+
+def _c_layout(struct, fields):
+    """sizeof + offsetof of a header struct, from a C program compiled with gcc."""
+    import shutil
+    import subprocess
+    import tempfile
+
+    if not shutil.which("gcc"):
+        pytest.skip("gcc is absent")
+    body = "".join(f'printf("%zu ", offsetof({struct}, {f}));' for f in fields)
+    src = ("#include <stdio.h>\n#include <stddef.h>\n#include \"mapple_b200.h\"\n"
+           f"int main(void){{printf(\"%zu \", sizeof({struct}));{body}return 0;}}\n")
+    with tempfile.TemporaryDirectory() as d:
+        c, exe = Path(d) / "l.c", Path(d) / "l"
+        c.write_text(src)
+        subprocess.run(["gcc", "-I", str(ROOT / "include"), "-I", "/usr/local/cuda/include",
+                        str(c), "-o", str(exe)], check=True, capture_output=True)
+        return [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                               check=True).stdout.split()]
+
+
+def test_ctypes_structs_match_the_header_layout():
+    """Every view struct the Python side builds has the C header's size and offsets
+    (the stencil / hydro views and the step ops changed shape in round 2)."""
+    import ctypes
+
+    from paper_2507_17087_b200.executors.circuit import PmCircuitView
+    from paper_2507_17087_b200.executors.hydro import PmHydroView
+    from paper_2507_17087_b200.executors.stencil import PmStencilView
+    from paper_2507_17087_b200.peer import PmPeerBarrierView, PmPeerCopy, PmStepOp
+
+    renames = {"in_": "in"}
+    for struct, cls in (("pm_step_op", PmStepOp), ("pm_stencil_view", PmStencilView),
+                        ("pm_hydro_view", PmHydroView), ("pm_circuit_view", PmCircuitView),
+                        ("pm_peer_barrier_view", PmPeerBarrierView),
+                        ("pm_peer_copy", PmPeerCopy), ("pm_program", native.PmProgram),
+                        ("pm_insn", native.PmInsn)):
+        names = [f[0] for f in cls._fields_]
+        want = _c_layout(struct, [renames.get(n, n) for n in names])
+        got = [ctypes.sizeof(cls)] + [getattr(cls, n).offset for n in names]
+        assert got == want, (struct, list(zip(["sizeof"] + names, got, want)))

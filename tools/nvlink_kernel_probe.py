@@ -11,7 +11,9 @@ every kernel (no cross-process barriers) and report its NVLink bytes
                   stencil/gemm counters only; timed here);
   stencil_peer    pm_stencil_sweep on GPU 0 whose down neighbour's rows and right
                   neighbour's column strip live on GPU 1 (sweep 0: no flag waits):
-                  4 B per halo cell read.
+                  4 B per halo cell read;
+  hydro_peer_zones the zone kernel on GPU 0 with every point on GPU 1: 16-byte
+                  point-state loads and 2 x 4-byte force atomics per corner.
 
     ncu --metrics nvlrx__bytes_data_user.sum,nvltx__bytes_data_user.sum,gpu__time_duration.sum \
         python tools/nvlink_kernel_probe.py
@@ -104,6 +106,42 @@ def main():
         torch.cuda.synchronize(0)
     out["stencil_peer"] = {"rect": [R, Cc], "halo_cells_read": 2 * R,
                            "algorithmic_nvlink_bytes": 4 * 2 * R}
+    # 4. hydro zones on GPU 0 whose points all live on GPU 1: every corner is a 16-byte
+    #    peer load of the point state and two 4-byte peer float atomics of its force
+    from paper_2507_17087_b200.executors.hydro import PmHydroView
+
+    Lx = Ly = 1024
+    nz, npt = Lx * Ly, (Lx + 1) * (Ly + 1)
+    zi = torch.arange(nz, device="cuda:0") % Lx
+    zj = torch.arange(nz, device="cuda:0") // Lx
+    W = Lx + 1
+    corners = [zj * W + zi, zj * W + zi + 1, (zj + 1) * W + zi + 1, (zj + 1) * W + zi]
+    z2p = torch.stack([(1 << 27) | c for c in corners]).to(torch.int32).contiguous()
+    zm = torch.full((nz,), 1.0 / nz, device="cuda:0")
+    ze = torch.ones(nz, device="cuda:0")
+    za = torch.full((nz,), 1.0 / nz, device="cuda:0")
+    zpe = torch.zeros(nz, device="cuda:0")
+    pst = torch.zeros(npt, 4, device="cuda:1")
+    pst[:, 0] = (torch.arange(npt, device="cuda:1") % W).float() / Lx
+    pst[:, 1] = (torch.arange(npt, device="cuda:1") // W).float() / Ly
+    fxy = torch.zeros(2 * npt, device="cuda:1")
+    hv = PmHydroView()
+    hv.n_zones, hv.n_points = nz, 0
+    hv.z2p, hv.zm, hv.ze, hv.za, hv.zpe = (z2p.data_ptr(), zm.data_ptr(), ze.data_ptr(),
+                                           za.data_ptr(), zpe.data_ptr())
+    hv.pm = hv.pbc = None
+    hv.pst[1], hv.fxy[1] = pst.data_ptr(), fxy.data_ptr()
+    hv.rank, hv.dt, hv.gamma, hv.cq = 0, 1e-6, 5.0 / 3.0, 1.0
+    torch.cuda.synchronize(1)
+    with torch.cuda.device(0):
+        s = native.stream_ptr(torch.cuda.current_stream(0))
+        for _ in range(2):
+            native.check(lib.pm_hydro_step(ctypes.byref(hv), 0, s), "pm_hydro_step")
+        torch.cuda.synchronize(0)
+    out["hydro_peer_zones"] = {"zones": nz, "points_on_peer": npt,
+                               "algorithmic_rx_bytes": 16 * 4 * nz,
+                               "algorithmic_rx_bytes_unique_points": 16 * npt,
+                               "algorithmic_tx_atomic_bytes": 8 * 4 * nz}
     print(json.dumps(out))
 
 
