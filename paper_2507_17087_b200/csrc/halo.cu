@@ -305,6 +305,9 @@ constexpr int kStripRows = 64;                 // rows per block (one mask bit e
 #ifndef PM_STRIP_MINB
 #define PM_STRIP_MINB 4
 #endif
+#ifndef PM_STRIP_PREFETCH
+#define PM_STRIP_PREFETCH 0
+#endif
 constexpr int kStripBatch = PM_STRIP_BATCH;    // rows of loads in flight per thread
 static_assert(kStripRows % kStripBatch == 0, "the unclamped walk takes whole batches");
 
@@ -382,6 +385,15 @@ __device__ __forceinline__ void strip_walk(const Strip2D& h, long long r0, int n
       }
     }
     if constexpr (!kClamp) {
+#if PM_STRIP_PREFETCH > 0
+      // L2 prefetch PM_STRIP_PREFETCH rows past this batch (one lane per 128-byte line):
+      // more bytes in flight than the register window holds, at no register cost
+      if ((lane & 7) == 0 && i + kStripBatch + PM_STRIP_PREFETCH < nr) {
+#pragma unroll
+        for (int u = 0; u < kStripBatch; ++u)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pr + (PM_STRIP_PREFETCH + u) * st));
+      }
+#endif
       pr += kStripBatch * st;
       pe += kStripBatch * st;
     }
