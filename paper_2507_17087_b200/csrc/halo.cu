@@ -306,7 +306,7 @@ constexpr int kStripRows = 64;                 // rows per block (one mask bit e
 #define PM_STRIP_MINB 4
 #endif
 #ifndef PM_STRIP_PREFETCH
-#define PM_STRIP_PREFETCH 0
+#define PM_STRIP_PREFETCH 4
 #endif
 constexpr int kStripBatch = PM_STRIP_BATCH;    // rows of loads in flight per thread
 static_assert(kStripRows % kStripBatch == 0, "the unclamped walk takes whole batches");
