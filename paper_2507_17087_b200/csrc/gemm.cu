@@ -177,6 +177,8 @@ struct Params {
                       // draw ticket_end - 1 is the last and zeroes the counter
   int k_split;        // 1-SM kernel: K slices per output tile (<= 1: none); > 1 adds
                       // every slice's partial product into C with vector red.add
+  int wave_slack;     // wave barrier: proceed when all but this many tiles of the
+                      // previous wave have issued their last load
   int wave_sync;      // wide kernel: a tile of wave w (= ticket / pairs) starts loading
                       // only once every tile of wave w - 1 has issued its last load
                       // (tile_counter[1] counts them): the co-resident tiles then walk K
@@ -922,7 +924,7 @@ k_gemm_bf16_wide(const __grid_constant__ CUtensorMap map_a,
           // wave barrier: every tile of the previous wave has issued its last load.  A
           // hint, not a correctness condition: a pair gives up after 2 ms (e.g. when
           // another kernel keeps some pairs from being resident), so it cannot hang
-          const int need = (t / npairs) * npairs;
+          const int need = (t / npairs) * npairs - p.wave_slack;
           volatile int* done = p.tile_counter + 1;
           if (*done < need) {
             unsigned long long t0, t1;
@@ -1305,6 +1307,7 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
       if (rc) return rc;
       p.ticket_end = (int)(pairs_needed + pairs);
       p.wave_sync = wave ? 1 : 0;
+      p.wave_slack = getenv("PM_GEMM_WAVE_SLACK") ? atoi(getenv("PM_GEMM_WAVE_SLACK")) : 0;
       PM_CUDA_TRY(cudaMemsetAsync(p.tile_counter, 0, 2 * sizeof(int), (cudaStream_t)stream));
       wide::k_gemm_bf16_wide<<<(unsigned)(2 * pairs), wide::kThreadsW, wide::SMEMW,
                                (cudaStream_t)stream>>>(ma, mb, mc, p);
