@@ -43,6 +43,7 @@ struct HaloKey {
   static constexpr bool kVec4 = true;
   static constexpr bool kPeek = false;
   __device__ __forceinline__ void uniform(long long, int, int) const {}
+  __device__ __forceinline__ void prefetch(long long, long long) const {}
   // the four slots (up, down, left, right) of cell i / 4 of a 2-D grid: one index
   // decomposition and one owner load per cell, neighbours from L1/L2
   __device__ __forceinline__ int keys4(long long i) const {

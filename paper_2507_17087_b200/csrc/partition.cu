@@ -33,6 +33,11 @@ struct ProcKey {
     return b;
   }
   __device__ __forceinline__ int operator()(long long i) const { return check(__ldg(proc + i), i); }
+  // L2 prefetch of the 128-byte line holding item i (the histogram pass prefetches the
+  // tile a CTA that starts about one CTA lifetime later will read)
+  __device__ __forceinline__ void prefetch(long long i, long long n) const {
+    if (i < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(proc + i));
+  }
   // four consecutive ids (i % 4 == 0) packed as int8 bins
   __device__ __forceinline__ int keys4(long long i) const {
     const int4 v = __ldg(reinterpret_cast<const int4*>(proc + i));
