@@ -8,7 +8,8 @@
 // points owned by another GPU) and deposits its corner forces with 8-byte float2 atomics straight into the
 // owning GPU's force array -- Legion PENNANT's master/ghost point exchange
 // and its point-force reduction become the cross-GPU corners of the zone
-// kernel, with no copy pass.
+// kernel, with no copy pass.  Corners shared by consecutive zones of a warp are summed
+// with shuffles first (about 2 atomics per zone on a row-numbered mesh).
 //
 //   k_hydro_zones   one thread per zone: area (shoelace), PdV energy update
 //                   with the previous step's pressure, EOS (gamma-law gas),
@@ -36,12 +37,12 @@ struct HydroArgs {
 __device__ __forceinline__ int rk(int ref) { return (int)((unsigned)ref >> 27); }
 __device__ __forceinline__ int sl(int ref) { return ref & ((1 << 27) - 1); }
 
-// one zone: area, PdV energy update, EOS, artificial viscosity, corner forces
-// deposited into the owners' force arrays (ref[k]: the zone's point references,
-// q[k]: their (x, y, u, v))
-__device__ __forceinline__ void hydro_zone(const pm_hydro_view& v, const int (&ref)[4],
-                                           const float4 (&st)[4], float zm, float ze, float za,
-                                           float zpe, float& e_out, float& a_out, float& pe_out) {
+// one zone: area, PdV energy update, EOS, artificial viscosity and the 4 corner forces
+// (st[k]: the (x, y, u, v) of the zone's point k; f[k]: point k's corner force)
+__device__ __forceinline__ void hydro_zone(const pm_hydro_view& v, const float4 (&st)[4],
+                                           float zm, float ze, float za, float zpe,
+                                           float2 (&f)[4], float& e_out, float& a_out,
+                                           float& pe_out) {
   float area = 0.f, dadt = 0.f;
   float nx[4], ny[4];  // edge k (point k -> k+1) outward normal scaled by its length
 #pragma unroll
@@ -63,21 +64,24 @@ __device__ __forceinline__ void hydro_zone(const pm_hydro_view& v, const int (&r
   e_out = e;
   a_out = area;
   pe_out = pe;
-  // corner force of point k = half of each adjacent edge's pressure force, deposited
-  // in the owner's memory: one 8-byte vector atomic (sm_90+ float2 atomicAdd) into
-  // this GPU's points; two 4-byte float atomics -- the form NVLink peer atomics
-  // natively support -- into a peer's
+  // corner force of point k = half of each adjacent edge's pressure force
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int km = (k + 3) & 3;
-    const int r = rk(ref[k]), s = sl(ref[k]);
-    const float fx = 0.5f * pe * (nx[km] + nx[k]), fy = 0.5f * pe * (ny[km] + ny[k]);
-    if (r == v.rank) {
-      atomicAdd(reinterpret_cast<float2*>(v.fxy[r]) + s, make_float2(fx, fy));
-    } else {
-      atomicAdd(v.fxy[r] + 2 * s, fx);
-      atomicAdd(v.fxy[r] + 2 * s + 1, fy);
-    }
+    f[k] = make_float2(0.5f * pe * (nx[km] + nx[k]), 0.5f * pe * (ny[km] + ny[k]));
+  }
+}
+
+// deposit a corner force in the owner's memory: one 8-byte vector atomic (sm_90+ float2
+// atomicAdd) into this GPU's points; two 4-byte float atomics -- the form NVLink peer
+// atomics natively support -- into a peer's
+__device__ __forceinline__ void deposit(const pm_hydro_view& v, int ref, float2 f) {
+  const int r = rk(ref), s = sl(ref);
+  if (r == v.rank) {
+    atomicAdd(reinterpret_cast<float2*>(v.fxy[r]) + s, f);
+  } else {
+    atomicAdd(v.fxy[r] + 2 * s, f.x);
+    atomicAdd(v.fxy[r] + 2 * s + 1, f.y);
   }
 }
 
@@ -87,23 +91,62 @@ __device__ __forceinline__ float4 point_state(const pm_hydro_view& v, int ref) {
   return __ldg(reinterpret_cast<const float4*>(v.pst[rk(ref)]) + sl(ref));
 }
 
+#ifndef PM_HYDRO_WARP_COMBINE
+#define PM_HYDRO_WARP_COMBINE 1
+#endif
+
+// One zone per thread.  Consecutive zones of a row share an edge: corners 1 and 2 of
+// zone z are corners 0 and 3 of zone z + 1 whenever the mesh numbers zones along rows
+// (checked per pair at run time, so any z2p is handled).  Each lane hands its corners
+// 1 / 2 to the next lane, which adds them to its corners 0 / 3 when the point refs
+// match: about 2 force atomics per zone instead of 4 on the L2 atomic units.
 __global__ void __launch_bounds__(256)
 k_hydro_zones(const __grid_constant__ HydroArgs a) {
   const pm_hydro_view& v = a.v;
   const long long z = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nz = v.n_zones;
-  if (z >= nz) return;
-  int ref[4];
-  float4 st[4];
+  const bool live = z < nz;
+#if !PM_HYDRO_WARP_COMBINE
+  if (!live) return;
+#endif
+  int ref[4] = {-1, -1, -1, -1};
+  float2 f[4];
+  if (live) {
+    float4 st[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) ref[k] = __ldg(v.z2p + k * nz + z);
+    for (int k = 0; k < 4; ++k) ref[k] = __ldg(v.z2p + k * nz + z);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) st[k] = point_state(v, ref[k]);
-  float e, ar, pe;
-  hydro_zone(v, ref, st, __ldg(v.zm + z), v.ze[z], v.za[z], v.zpe[z], e, ar, pe);
-  v.ze[z] = e;
-  v.za[z] = ar;
-  v.zpe[z] = pe;
+    for (int k = 0; k < 4; ++k) st[k] = point_state(v, ref[k]);
+    float e, ar, pe;
+    hydro_zone(v, st, __ldg(v.zm + z), v.ze[z], v.za[z], v.zpe[z], f, e, ar, pe);
+    v.ze[z] = e;
+    v.za[z] = ar;
+    v.zpe[z] = pe;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) f[k] = make_float2(0.f, 0.f);
+  }
+#if PM_HYDRO_WARP_COMBINE
+  const unsigned all = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int r1 = __shfl_up_sync(all, ref[1], 1), r2 = __shfl_up_sync(all, ref[2], 1);
+  const float g1x = __shfl_up_sync(all, f[1].x, 1), g1y = __shfl_up_sync(all, f[1].y, 1);
+  const float g2x = __shfl_up_sync(all, f[2].x, 1), g2y = __shfl_up_sync(all, f[2].y, 1);
+  const bool take0 = live && lane > 0 && r1 == ref[0];
+  const bool take3 = live && lane > 0 && r2 == ref[3];
+  if (take0) f[0].x += g1x, f[0].y += g1y;
+  if (take3) f[3].x += g2x, f[3].y += g2y;
+  const bool gave1 = __shfl_down_sync(all, take0, 1) && lane < 31;
+  const bool gave2 = __shfl_down_sync(all, take3, 1) && lane < 31;
+  if (!live) return;
+  deposit(v, ref[0], f[0]);
+  if (!gave1) deposit(v, ref[1], f[1]);
+  if (!gave2) deposit(v, ref[2], f[2]);
+  deposit(v, ref[3], f[3]);
+#else
+#pragma unroll
+  for (int k = 0; k < 4; ++k) deposit(v, ref[k], f[k]);
+#endif
 }
 
 __device__ __forceinline__ float4 hydro_move(float4 q, float2 f, float m, int bc, float dt) {
@@ -158,6 +201,8 @@ int pm_hydro_step(const pm_hydro_view* view, int32_t phase, void* stream) {
     if (view->n_zones == 0) return PM_OK;
     // one zone per thread (two per thread, with vector zone loads and eight gathers in
     // flight, was slower: 1.21 vs 0.96 ms at 67M zones)
+    // (two vertically stacked zones per thread over a row-pair zone numbering -- 6 gathers
+    // and 1.5 atomics per zone -- measured slower: 1.10 vs 0.92 ms, tools/hydro_ab2.sh)
     pm::k_hydro_zones<<<(unsigned)((view->n_zones + 255) / 256), 256, 0, s>>>(a);
   } else if (phase == 1) {
     if (view->n_points == 0) return PM_OK;
