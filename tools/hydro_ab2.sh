@@ -1,3 +1,4 @@
+# (historical: the PM_HYDRO_PAIRS kernel and zone reorder were removed after this A/B)
 # A/B: one zone per thread with row shuffle merge (default) vs row-pair zones (PM_HYDRO_PAIRS=1),
 # vs no merge (var_hz0); then the hydro parity checks under the pairs kernel.
 out=gpurun_out/hydro_ab2.txt
