@@ -121,12 +121,21 @@ def init_dist(n_gpus: int):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != n_gpus:
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}; launch with torchrun for N>1")
+    # PM_BENCH_OVERSUB=1 (a code-path check, never a measurement): more ranks than GPUs,
+    # ranks sharing a GPU through same-device IPC, gloo instead of NCCL (NCCL refuses two
+    # ranks on one GPU) -- how an 8-rank run is exercised on a 4-GPU box
+    oversub = os.environ.get("PM_BENCH_OVERSUB", "0") != "0"
+    if oversub:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
