@@ -539,32 +539,49 @@ def run_e2e_pipelined_multi(args, ex, rank, world):
         for k in ("comp", "free", "out"):
             ev[k][b].record(cs)
 
+    trace = [] if os.environ.get("PM_E2E_TRACE") else None
+
+    def mark(stream):
+        if trace and trace[-1] is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            trace[-1].append(e)
+
     def run(n, t0=None, t1=None):
         if t0 is not None:
             t0.record(h2d)
         for s in range(n):
             b = s % 2
             E = sets[b]
+            if trace is not None:
+                trace.append([] if t0 is not None else None)
             h2d.wait_event(ev["free"][b])      # every GPU done pulling from set b
+            mark(h2d)
             with torch.cuda.stream(h2d):
                 E.A[:, ka[0]:ka[1]].copy_(hA, non_blocking=True)
                 E.Bt[:, kb[0]:kb[1]].copy_(hB, non_blocking=True)
             ev["in"][b].record(h2d)
+            mark(h2d)
             comm.wait_event(ev["in"][b])
             with torch.cuda.stream(comm):     # every GPU's slices of set b landed
                 dist.all_reduce(flag[0:1])
             ev["ready"][b].record(comm)
             cs.wait_event(ev["out"][b])        # C of two steps ago has been read out
+            cs.wait_event(ev["ready"][b])
+            mark(cs)
             E.step(stream=cs, ready=ev["ready"][b])
             ev["comp"][b].record(cs)
+            mark(cs)
             comm.wait_event(ev["comp"][b])
             with torch.cuda.stream(comm):
                 dist.all_reduce(flag[1:2])
             ev["free"][b].record(comm)
             d2h.wait_event(ev["comp"][b])
+            mark(d2h)
             with torch.cuda.stream(d2h):
                 hC[b].copy_(E.C, non_blocking=True)
             ev["out"][b].record(d2h)
+            mark(d2h)
         if t1 is not None:
             t1.record(d2h)
 
@@ -576,6 +593,9 @@ def run_e2e_pipelined_multi(args, ex, rank, world):
     run(n, t0, t1)
     torch.cuda.synchronize()
     ms = max_over_ranks(t0.elapsed_time(t1) / n, world)
+    if trace is not None and rank == 0:  # per step: h2d, compute, d2h (start, end) in ms
+        tr = [[round(t0.elapsed_time(e), 2) for e in st] for st in trace if st is not None]
+        print(json.dumps({"e2e_trace": tr[:12]}), file=sys.stderr)
     barrier(world)
     ex2.close()
     del ex2
