@@ -1226,12 +1226,10 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
   // so a 4-row raster group shares A panels across ~18 tiles and B panels across 4 while
   // they are in L2 (32768^3: 97 -> 52 GB DRAM reads, +9% clock under the power cap,
   // 1290 -> 1412 TF/s sustained, cuBLAS 1328); without it narrow groups re-read less
-  // A reduce-adding launch (C in a peer's memory: the 3-D / 2.5D fused reduce-scatter) runs
-  // without it: wave-aligned tiles would all drain over NVLink at once, stalling the MMAs
-  // behind the remote epilogues (Johnson 32768^3 (1,2,2) at N=4: 13.19 -> 12.92 ms,
-  // tools/grid3d_ab.sh)
-  const bool wave = kind == 2 && !atomic_add &&
-                    !(getenv("PM_GEMM_WAVESYNC") && atoi(getenv("PM_GEMM_WAVESYNC")) == 0);
+  // (reduce-adding launches -- C in a peer's memory -- measured the same with and without
+  // it, and with half a wave of slack: Johnson (1,1,2) / (1,2,2) within +-2% run to run,
+  // tools/grid3d_ab2.sh)
+  const bool wave = kind == 2 && !(getenv("PM_GEMM_WAVESYNC") && atoi(getenv("PM_GEMM_WAVESYNC")) == 0);
   p.group_m = kind == 2 ? (wave ? 4 : (K >= 24576 ? 2 : 4)) : 8;
   if (const char* g = getenv("PM_GEMM_GROUP")) p.group_m = atoi(g) > 0 ? atoi(g) : p.group_m;
   p.debug_nostore = getenv("PM_GEMM_NOSTORE") ? 1 : 0;

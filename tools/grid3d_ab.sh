@@ -1,3 +1,4 @@
+# (historical: the PM_GEMM_ADD_* knobs were removed after this A/B -- no difference beyond noise)
 # A/B at N=4 of GEMM knobs for the reduce-adding 3-D grids (tools/grid3d_probe.py)
 out=gpurun_out/grid3d_ab.txt
 : > $out

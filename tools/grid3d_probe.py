@@ -17,8 +17,12 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
     out = {"world": world, "env": {k: v for k, v in os.environ.items() if k.startswith("PM_")}}
     shapes = {"johnson": (32768, 32768, 32768), "cosma": (65536, 16384, 16384)}
+    only = os.environ.get("PROBE_SHAPES")
+    if only:
+        shapes = {k: v for k, v in shapes.items() if k in only.split(",")}
+    maps = os.environ.get("PROBE_MAPPINGS", "decompose,heuristic").split(",")
     for name, (M, N, K) in shapes.items():
-        for mapping in ("decompose", "heuristic"):
+        for mapping in maps:
             ex = MappedGemm3D(M, N, K, mapping=mapping, rank=rank, world=world, seed=99)
             for _ in range(3):
                 ex.step()
