@@ -114,8 +114,9 @@ int pm_map_scatter(pm_plan* plan, const int32_t* points, int64_t n, int64_t firs
   const void* dst = bin_dst ? (const void*)bin_dst : (const void*)perm;
   void* args[] = {(void*)&pts, (void*)&nn, (void*)&ff, (void*)&nb, (void*)&ntiles,
                   (void*)&pos0, (void*)&status, (void*)&out_proc, (void*)&dst, (void*)&base};
-  PM_CU_TRY(d->launchKernel(f, (unsigned)ntiles, 1, 1, pm::kPartThreads, 1, 1, (unsigned)smem,
-                            (CUstream)stream, args, nullptr));
+  // (the NVRTC text and this file see the same PM_SCATTER_TILES default)
+  PM_CU_TRY(d->launchKernel(f, pm::small_scatter_grid(ntiles), 1, 1, pm::kPartThreads, 1, 1,
+                            (unsigned)smem, (CUstream)stream, args, nullptr));
   return PM_OK;
 }
 

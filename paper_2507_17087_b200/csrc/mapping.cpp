@@ -566,8 +566,9 @@ pm_map_scatter(const int* pts, long long n, long long first, int nbins, long lon
                int* perm, long long base) {
   extern __shared__ __align__(16) int smem_words[];
   const PmMapKey key{pts, first, status, out, nbins};
-  pmdev::small_scatter_body(key, PmPermSink{perm, base}, n, nbins, ntiles, pos0, smem_words,
-                            (long long)blockIdx.x);
+  pmdev::small_scatter_tiles<pmdev::kScatterTiles>(key, PmPermSink{perm, base}, n, nbins, ntiles, pos0,
+                                                   smem_words,
+                                                   (long long)blockIdx.x * pmdev::kScatterTiles);
 }
 
 extern "C" __global__ void __launch_bounds__(256, 6)
@@ -576,8 +577,9 @@ pm_map_scatter_peer(const int* pts, long long n, long long first, int nbins, lon
                     const long long* tab, long long base) {
   extern __shared__ __align__(16) int smem_words[];
   const PmMapKey key{pts, first, status, out, nbins};
-  pmdev::small_scatter_body(key, PmPeerSink{tab, base}, n, nbins, ntiles, pos0, smem_words,
-                            (long long)blockIdx.x);
+  pmdev::small_scatter_tiles<pmdev::kScatterTiles>(key, PmPeerSink{tab, base}, n, nbins, ntiles, pos0,
+                                                   smem_words,
+                                                   (long long)blockIdx.x * pmdev::kScatterTiles);
 }
 )CUDA";
 
@@ -606,8 +608,10 @@ int nvrtc_compile(const std::string& src, std::vector<char>* cubin, bool with_pa
                          with_partition ? hdr_src : nullptr,
                          with_partition ? hdr_name : nullptr) != NVRTC_SUCCESS)
     return set_error("nvrtcCreateProgram failed"), PM_ERR_NVRTC;
+#define PM_STR2(x) #x
+#define PM_STR(x) PM_STR2(x)
   const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-device-int128", "-lineinfo",
-                        "-default-device", "-w"};
+                        "-default-device", "-w", "-DPM_SCATTER_TILES=" PM_STR(PM_SCATTER_TILES)};
   nvrtcResult rc = nvrtcCompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
   if (rc != NVRTC_SUCCESS) {
     size_t n = 0;

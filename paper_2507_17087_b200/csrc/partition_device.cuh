@@ -32,6 +32,10 @@ constexpr int kSmallBins = 64;
 constexpr int kIPT = 16;                          // items per thread
 constexpr int kSmallTile = kPartThreads * kIPT;   // 4096 items per tile
 
+#ifndef PM_IOTA_CS
+#define PM_IOTA_CS 1
+#endif
+
 // dst[k] = v0 + k for k < count, by the whole CTA: 16-byte streaming stores
 // between a scalar head (to 16-byte alignment) and tail.
 __device__ __forceinline__ void store_iota(int* dst, int v0, int count) {
@@ -42,8 +46,12 @@ __device__ __forceinline__ void store_iota(int* dst, int v0, int count) {
   int4* body = reinterpret_cast<int4*>(dst + head);
   for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
     const int e = v0 + head + 4 * v;
+#if PM_IOTA_CS
     asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(body + v), "r"(e),
                  "r"(e + 1), "r"(e + 2), "r"(e + 3) : "memory");
+#else
+    body[v] = make_int4(e, e + 1, e + 2, e + 3);
+#endif
   }
   for (int k = head + 4 * nvec + threadIdx.x; k < count; k += blockDim.x) dst[k] = v0 + k;
 }
@@ -334,6 +342,53 @@ __device__ __forceinline__ void small_scatter_body(const Key& key, const Sink& s
     if (lo == hi) continue;
     const long long p0 = pos0[(long long)b * ntiles + tile] - lo;
     for (int k = lo + lane; k < hi; k += 32) sink.put(b, p0 + k, base + stage[k]);
+  }
+}
+
+// The scatter over kTiles consecutive tiles (first_tile ..) per CTA.  The prologue
+// fetches every tile's summary and -- in parallel, not after it -- all nbins candidate
+// output starts, so a uniform tile's stores wait for one load latency instead of two
+// dependent ones, once per kTiles tiles.  Mixed tiles take the general body.
+#ifndef PM_SCATTER_TILES
+#define PM_SCATTER_TILES 2
+#endif
+constexpr int kScatterTiles = PM_SCATTER_TILES;
+
+template <int kTiles, class Key, class Sink>
+__device__ __forceinline__ void small_scatter_tiles(const Key& key, const Sink& sink, long long n,
+                                                    int nbins, long long ntiles,
+                                                    const long long* __restrict__ pos0,
+                                                    int* smem_words, long long first_tile) {
+  __shared__ int s_info[kTiles];
+  __shared__ long long s_p0[kTiles][kSmallBins];
+  const int* tile_info = tile_info_of(pos0, nbins, ntiles);
+  const int per = nbins + 1;
+  if (kTiles * per <= kPartThreads) {
+    const int j = threadIdx.x / per, q = threadIdx.x - j * per;
+    const long long t = first_tile + j;
+    if (j < kTiles) {
+      if (q == nbins) s_info[j] = t < ntiles ? __ldg(tile_info + t) : kTileEmpty;
+      else if (t < ntiles) s_p0[j][q] = __ldg(pos0 + (long long)q * ntiles + t);
+    }
+  } else if (threadIdx.x < kTiles) {
+    const long long t = first_tile + threadIdx.x;
+    const int info = t < ntiles ? __ldg(tile_info + t) : kTileEmpty;
+    s_info[threadIdx.x] = info;
+    if (info >= 0) s_p0[threadIdx.x][info] = __ldg(pos0 + (long long)info * ntiles + t);
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int j = 0; j < kTiles; ++j) {
+    const long long t = first_tile + j;
+    const int info = s_info[j];
+    if (info == kTileEmpty) continue;
+    if (info >= 0) {
+      key.uniform(t * kSmallTile, kSmallTile, info);
+      sink.put_run(info, s_p0[j][info], t * kSmallTile, kSmallTile);
+      continue;
+    }
+    small_scatter_body(key, sink, n, nbins, ntiles, pos0, smem_words, t);
+    __syncthreads();  // shared memory is reused by the next mixed tile
   }
 }
 

@@ -3,6 +3,12 @@
 // loads on machines without libcuda -- the CPU build/test container).
 #pragma once
 
+// tiles per CTA of the partition scatter (partition_device.cuh keeps the same default for
+// NVRTC, and mapping.cpp passes this value to every NVRTC compile)
+#ifndef PM_SCATTER_TILES
+#define PM_SCATTER_TILES 2
+#endif
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 

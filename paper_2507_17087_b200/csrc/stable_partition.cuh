@@ -144,13 +144,17 @@ k_small_hist(Key key, long long n, int nbins, long long ntiles, long long* __res
 }
 
 // (min 6 CTAs / SM: the uniform-tile copy is a pure store stream, occupancy-bound)
+// kScatterTiles tiles per CTA (partition_device.cuh small_scatter_tiles)
 template <class Key, class Sink>
 __global__ void __launch_bounds__(kPartThreads, 6)
 k_small_scatter(Key key, Sink sink, long long n, int nbins, long long ntiles,
                 const long long* __restrict__ pos0) {
   extern __shared__ __align__(16) int smem_words[];
-  pmdev::small_scatter_body(key, sink, n, nbins, ntiles, pos0, smem_words,
-                            (long long)blockIdx.x);
+  pmdev::small_scatter_tiles<pmdev::kScatterTiles>(key, sink, n, nbins, ntiles, pos0, smem_words,
+                                                   (long long)blockIdx.x * pmdev::kScatterTiles);
+}
+inline unsigned small_scatter_grid(long long ntiles) {
+  return (unsigned)((ntiles + pmdev::kScatterTiles - 1) / pmdev::kScatterTiles);
 }
 
 inline size_t small_hist_smem(int nbins) {
@@ -189,7 +193,7 @@ int stable_partition_small(Key key, Sink sink, bool scatter, long long n, int nb
       hist, ntiles, nbins, reinterpret_cast<const long long*>(scan_tmp), counts, offsets);
   PM_CUDA_TRY(cudaGetLastError());
   if (scatter) {
-    k_small_scatter<Key, Sink><<<(unsigned)ntiles, kPartThreads, smem_s, s>>>(
+    k_small_scatter<Key, Sink><<<small_scatter_grid(ntiles), kPartThreads, smem_s, s>>>(
         key, sink, n, nbins, ntiles, hist);
     PM_CUDA_TRY(cudaGetLastError());
   }
@@ -212,7 +216,7 @@ int stable_partition_small_scatter(Key key, Sink sink, long long n, int nbins, v
   if (smem_s > 48 * 1024)
     PM_CUDA_TRY(cudaFuncSetAttribute(k_small_scatter<Key, Sink>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
-  k_small_scatter<Key, Sink><<<(unsigned)ntiles, kPartThreads, smem_s, s>>>(
+  k_small_scatter<Key, Sink><<<small_scatter_grid(ntiles), kPartThreads, smem_s, s>>>(
       key, sink, n, nbins, ntiles, reinterpret_cast<const long long*>(scratch));
   PM_CUDA_TRY(cudaGetLastError());
   return PM_OK;
