@@ -42,6 +42,7 @@ struct HaloKey {
   bool div_one;           // ext[1] == 1
   static constexpr bool kVec4 = true;
   static constexpr bool kPeek = false;
+  static constexpr bool kRaw4 = false;
   __device__ __forceinline__ void uniform(long long, int, int) const {}
   __device__ __forceinline__ void prefetch(long long, long long) const {}
   // the four slots (up, down, left, right) of cell i / 4 of a 2-D grid: one index

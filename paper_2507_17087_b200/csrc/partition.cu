@@ -39,11 +39,15 @@ struct ProcKey {
     if (i < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(proc + i));
   }
   // four consecutive ids (i % 4 == 0) packed as int8 bins
-  __device__ __forceinline__ int keys4(long long i) const {
-    const int4 v = __ldg(reinterpret_cast<const int4*>(proc + i));
+  static constexpr bool kRaw4 = true;
+  __device__ __forceinline__ int4 raw4(long long i) const {
+    return __ldg(reinterpret_cast<const int4*>(proc + i));
+  }
+  __device__ __forceinline__ int pack4(int4 v, long long i) const {
     return (check(v.x, i) & 0xFF) | ((check(v.y, i + 1) & 0xFF) << 8) |
            ((check(v.z, i + 2) & 0xFF) << 16) | ((check(v.w, i + 3) & 0xFF) << 24);
   }
+  __device__ __forceinline__ int keys4(long long i) const { return pack4(raw4(i), i); }
 };
 
 struct PermSink {

@@ -10,6 +10,8 @@
 //               static constexpr bool kVec4; if true also
 //               bool vec_ok; int keys4(long long i) -> 4 int8 bins of items i..i+3
 //               void prefetch(long long i, long long n): L2 prefetch of item i's key
+//               static constexpr bool kRaw4; if true also int4 raw4(long long i) (the
+//               16-byte load alone) and int pack4(int4, long long i) (keys4 of it)
 //               void uniform(long long base, int count, int bin): the scatter
 //               skipped evaluating items [base, base + count), all in `bin`
 //               static constexpr bool kPeek; if true also int peek(long long i):
@@ -136,16 +138,39 @@ __device__ __forceinline__ void small_hist_body(const Key& key, long long n, int
     if (threadIdx.x < kSmallTile / 32)
       key.prefetch(base + (long long)PM_HIST_PREFETCH_TILES * kSmallTile + 32 * threadIdx.x, n);
 #endif
+    if (base + kSmallTile <= n && key.vec_ok) {
+      // all four 16-byte loads first, then the counting: the loads are in flight
+      // together (interleaved with the counting, ptxas issued them one at a time)
+      int packed[kIPT / 4];
+      if constexpr (Key::kRaw4) {
+        int4 raw[kIPT / 4];
 #pragma unroll
-    for (int m = 0; m < kIPT / 4; ++m) {
-      const long long i = base + (long long)(m * kPartThreads + threadIdx.x) * 4;
-      if (i + 3 < n && key.vec_ok) {
-        const int packed = key.keys4(i);
+        for (int m = 0; m < kIPT / 4; ++m)
+          raw[m] = key.raw4(base + (long long)(m * kPartThreads + threadIdx.x) * 4);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) add((int)(signed char)(packed >> (8 * q)));
+        for (int m = 0; m < kIPT / 4; ++m)
+          packed[m] = key.pack4(raw[m], base + (long long)(m * kPartThreads + threadIdx.x) * 4);
       } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) add(i + q < n ? key(i + q) : -1);
+        for (int m = 0; m < kIPT / 4; ++m)
+          packed[m] = key.keys4(base + (long long)(m * kPartThreads + threadIdx.x) * 4);
+      }
+#pragma unroll
+      for (int m = 0; m < kIPT / 4; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) add((int)(signed char)(packed[m] >> (8 * q)));
+    } else {
+#pragma unroll
+      for (int m = 0; m < kIPT / 4; ++m) {
+        const long long i = base + (long long)(m * kPartThreads + threadIdx.x) * 4;
+        if (i + 3 < n && key.vec_ok) {
+          const int packed = key.keys4(i);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) add((int)(signed char)(packed >> (8 * q)));
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) add(i + q < n ? key(i + q) : -1);
+        }
       }
     }
   } else if (base + kSmallTile <= n) {  // full tile: no bounds checks
