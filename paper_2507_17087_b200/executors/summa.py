@@ -17,7 +17,9 @@ Execution (one step = one full multiply):
     column group straight from the peers' memory over NVLink with the copy
     engines (no SM cost, no NCCL kernel competing with the GEMM);
   * B first, then A in row chunks, so the tcgen05 GEMM (K4) of chunk r runs
-    while chunk r+1 is still in flight; C accumulates in TMEM over the full K.
+    while chunk r+1 is still in flight (a run whose A is local but B remote is
+    chunked along C's columns instead, so its first GEMM waits for one B chunk,
+    not all of B); C accumulates in TMEM over each run's K.
 """
 
 from __future__ import annotations
@@ -164,7 +166,7 @@ class PanelPlan:
     panels: list      # (k0, k1, A source rank, B source rank), in execution order
     chunks: list      # A row chunks of remote panels
     pulls: list       # (operand, source rank, row0, rows, k0, k1, stream index)
-    gemms: list       # (r0, r1, k0, k1, accumulate, [indices into pulls to wait for])
+    gemms: list       # (r0, r1, k0, k1, accumulate, [indices into pulls to wait for], c0, c1)
     n_streams: int
 
 
@@ -219,11 +221,15 @@ def plan_panels(layout: Layout, me: int, K: int, mr: int, nc: int, block: int = 
             runs.append([r])
     runs.sort(key=lambda run: (sum(r[0] for r in run), run[0][1]))
     runs.insert(0, head)
-    nbr = -(-mr // block)
-    n = max(1, min(a_chunks, nbr))
-    chunks = [(min(mr, nbr * c // n * block), min(mr, nbr * (c + 1) // n * block))
-              for c in range(n)]
-    chunks = [(a, b) for a, b in chunks if b > a]
+    def cut(extent):
+        nb = -(-extent // block)
+        n = max(1, min(a_chunks, nb))
+        out = [(min(extent, nb * c // n * block), min(extent, nb * (c + 1) // n * block))
+               for c in range(n)]
+        return [(a, b) for a, b in out if b > a]
+
+    chunks = cut(mr)        # A-row chunks (C rows) of runs that pull A
+    col_chunks = cut(nc)    # B-row chunks (C columns) of runs that pull only B
     n_streams = copy_streams if any(r[0] for r in ranked) else 0
     pulls, gemms = [], []
     rr = 0
@@ -240,16 +246,41 @@ def plan_panels(layout: Layout, me: int, K: int, mr: int, nc: int, block: int = 
             rr += 1
         return idx
 
+    # a run is chunked only when its pulls may still be in flight when it starts:
+    # every pull is issued at the step's start, so compare the bytes pulled up to and
+    # including this run (at a conservative 500 GB/s) with the GEMM time ahead of it
+    # (at 1.2 PFLOP/s); a run whose operands surely landed runs as one launch
+    pulled_bytes, prior_flops = 0, 0
     first = True
     for run in runs:
         k0, k1 = run[0][1], run[-1][2]
+        a_remote = any(a_src != me for _, _, _, a_src, _ in run)
+        b_remote = any(b_src != me for _, _, _, _, b_src in run)
+        pulled_bytes += 2 * sum(r[0] for r in run)
+        landed = pulled_bytes / 500e9 < prior_flops / 1.2e15
+        prior_flops += 2 * mr * nc * (k1 - k0)
+        if landed and (a_remote or b_remote):
+            evs = [i for _, p0, p1, a_src, b_src in run
+                   for i in ((pull("Bt", b_src, 0, nc, p0, p1) if b_src != me else []) +
+                             (pull("A", a_src, 0, mr, p0, p1) if a_src != me else []))]
+            gemms.append((0, mr, k0, k1, not first, evs, 0, nc))
+            first = False
+            continue
+        if b_remote and not a_remote:
+            # only B arrives over NVLink: chunk the run along C's columns, so the GEMM
+            # of column chunk c starts once that chunk's B rows landed (not all of B)
+            for c0, c1 in col_chunks:
+                b_evs = [i for _, p0, p1, _, b_src in run if b_src != me
+                         for i in pull("Bt", b_src, c0, c1 - c0, p0, p1)]
+                gemms.append((0, mr, k0, k1, not first, b_evs, c0, c1))
+            first = False
+            continue
         b_evs = [i for _, p0, p1, _, b_src in run if b_src != me
                  for i in pull("Bt", b_src, 0, nc, p0, p1)]
-        a_remote = any(a_src != me for _, _, _, a_src, _ in run)
         for r0, r1 in (chunks if a_remote else [(0, mr)]):
             a_evs = [i for _, p0, p1, a_src, _ in run if a_src != me
                      for i in pull("A", a_src, r0, r1 - r0, p0, p1)]
-            gemms.append((r0, r1, k0, k1, not first, b_evs + a_evs))
+            gemms.append((r0, r1, k0, k1, not first, b_evs + a_evs, 0, nc))
             b_evs = []  # later chunks of this run follow the first on one stream
         first = False
     ranked = [r for run in runs for r in run]
@@ -313,8 +344,8 @@ class MappedGemm:
                              for _ in range(plan.n_streams)]
         events = [torch.cuda.Event() for _ in plan.pulls]
         self.pulls = [p + (events[i],) for i, p in enumerate(plan.pulls)]
-        self.gemms = [(r0, r1, k0, k1, acc, [events[i] for i in evs])
-                      for r0, r1, k0, k1, acc, evs in plan.gemms]
+        self.gemms = [(r0, r1, k0, k1, acc, [events[i] for i in evs], c0, c1)
+                      for r0, r1, k0, k1, acc, evs, c0, c1 in plan.gemms]
         self.panels = plan.panels
         self.chunks = plan.chunks
 
@@ -352,12 +383,13 @@ class MappedGemm:
         c_bf16 = int(self.C.dtype != native.require_cuda().float32)
         csz = self.C.element_size()
         nc = self.C.shape[1]
-        for r0, r1, k0, k1, acc, evs in self.gemms:
+        for r0, r1, k0, k1, acc, evs, c0, c1 in self.gemms:
             for ev in evs:
                 prog.wait(at[ev_index[id(ev)]])
             prog.gemm_bf16(self.A.data_ptr() + (r0 * K + k0) * esz, K,
-                           self.Bt.data_ptr() + k0 * esz, K, self.C.data_ptr() + r0 * nc * csz,
-                           nc, r1 - r0, nc, k1 - k0, c_bf16, int(acc))
+                           self.Bt.data_ptr() + (c0 * K + k0) * esz, K,
+                           self.C.data_ptr() + (r0 * nc + c0) * csz, nc, r1 - r0, c1 - c0,
+                           k1 - k0, c_bf16, int(acc))
         progs[key] = prog.build()
         return prog
 
@@ -390,11 +422,11 @@ class MappedGemm:
             s = self.copy_streams[si]
             self._copy(name, q, row0, rows, k0, k1, s)
             ev.record(s)
-        for r0, r1, k0, k1, acc, evs in self.gemms:
+        for r0, r1, k0, k1, acc, evs, c0, c1 in self.gemms:
             for ev in evs:
                 cs.wait_event(ev)
-            tile_gemm(self.A[r0:r1, k0:k1], self.Bt[:, k0:k1], self.C[r0:r1], accumulate=acc,
-                      stream=cs)
+            tile_gemm(self.A[r0:r1, k0:k1], self.Bt[c0:c1, k0:k1], self.C[r0:r1, c0:c1],
+                      accumulate=acc, stream=cs)
         self.done.record(cs)
         return self.C
 
