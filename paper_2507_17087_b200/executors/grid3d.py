@@ -13,7 +13,8 @@ GPU (a, b, c) computes the partial product A[a, c] * B[c, b] over K block c:
     B[c, b]; the rest of both blocks is pulled from the peers of its
     n-group / m-group by the copy engines (all-gather, no SMs);
   * reduce-scatter over c: C[a, b] rows are split among the pk GPUs of the
-    k-group; the GEMM is launched once per destination row range and its
+    k-group; the GEMM is launched per destination row range (cut further where
+    operands arrive separately, plan_3d) and its
     epilogue reduce-adds the tile straight into the owner's C buffer over
     NVLink (TMA `cp.reduce.async.bulk.tensor .add` on an IPC-mapped pointer) --
     the collective is fused into the GEMM, there is no separate NCCL call.
@@ -65,6 +66,76 @@ def comm_bytes_3d(M, N, K, grid) -> dict:
             "total": int(a + b + c)}
 
 
+def plan_3d(grid, coord, owner, mb: int, nb: int, a_chunks: int = 4) -> dict:
+    """This GPU's step schedule (pure; CPU-testable).
+
+    Pulls: the A row parts of the n-group (each cut into `a_chunks` pieces) and the Bt
+    row parts (C columns) of the m-group, issued on ONE copy lane in the order the GEMMs
+    need them (peer copies on several lanes ran one lane after another, not at once).
+    GEMMs: every destination's rows (own first, then the peers') cut into sub-products
+    at the edges of what arrives separately -- A rows at the local part / pull chunks,
+    C columns at the Bt parts -- so the first product needs only operands already here
+    or the first pull, not the whole all-gather.  Returns {"pulls": [(name, src rank,
+    (r0, r1))], "gemms": [(rows, cols, dst rank, dst row0, [pull indices])],
+    "barrier_before": index of the first reduce-adding product (or None)}."""
+    pm, pn, pk = grid
+    a, b, c = coord
+    me = owner[(a, b, c)]
+    a_parts = []  # (rows, src) ; src None = local
+    for b2 in range(pn):
+        r = split(mb, pn, b2)
+        if b2 == b:
+            a_parts.append((r, None))
+        else:
+            n = max(1, min(a_chunks, (r[1] - r[0]) // 128))
+            for i in range(n):
+                a_parts.append(((r[0] + (r[1] - r[0]) * i // n, r[0] + (r[1] - r[0]) * (i + 1) // n),
+                                owner[(a, b2, c)]))
+    b_parts = [(split(nb, pm, a2), None if a2 == a else owner[(a2, b, c)]) for a2 in range(pm)]
+    local_first = sorted(range(len(a_parts)), key=lambda i: (a_parts[i][1] is not None, i))
+    col_order = sorted(range(len(b_parts)), key=lambda i: (b_parts[i][1] is not None, i))
+    pulls, pull_of = [], {}
+
+    def need(kind, i):
+        key = (kind, i)
+        if key not in pull_of:
+            rows, src = (a_parts if kind == "A" else b_parts)[i]
+            pull_of[key] = len(pulls)
+            pulls.append(("A" if kind == "A" else "Bt", src, rows))
+        return pull_of[key]
+
+    gemms, barrier_before = [], None
+    for d in [(c + i) % pk for i in range(pk)]:
+        R = split(mb, pk, d)
+        dst = owner[(a, b, d)]
+        if dst != me and barrier_before is None:
+            barrier_before = len(gemms)
+        for ai in local_first:
+            (r0, r1), asrc = a_parts[ai]
+            lo, hi = max(r0, R[0]), min(r1, R[1])
+            if lo >= hi:
+                continue
+            for bi in col_order:
+                (c0, c1), bsrc = b_parts[bi]
+                evs = ([need("A", ai)] if asrc is not None else []) + \
+                      ([need("B", bi)] if bsrc is not None else [])
+                gemms.append(((lo, hi), (c0, c1), dst, R[0], evs))
+    # merge column neighbours that wait for nothing new (fewer launches): a product over
+    # local columns right after another over the same rows and local columns
+    merged = []
+    for g in gemms:
+        if merged:
+            p = merged[-1]
+            if (p[0] == g[0] and p[2] == g[2] and p[1][1] == g[1][0] and
+                    set(g[4]) <= set(p[4])):
+                merged[-1] = (p[0], (p[1][0], g[1][1]), p[2], p[3], p[4])
+                continue
+        merged.append(g)
+    if barrier_before is not None:
+        barrier_before = next(i for i, g in enumerate(merged) if g[2] != me)
+    return {"pulls": pulls, "gemms": merged, "barrier_before": barrier_before}
+
+
 class MappedGemm3D:
     def __init__(self, M, N, K, *, mapping="decompose", rank=0, world=1, group=None, seed=0,
                  grid=None, block=256):
@@ -114,28 +185,13 @@ class MappedGemm3D:
                   for _ in range(2)]
         self.peers = PeerBuffers({"A": self.A, "Bt": self.Bt, "C0": self.C[0],
                                   "C1": self.C[1]}, rank, world, group)
-        self.streams = [torch.cuda.Stream(device=self.device) for _ in range(4)]
-        # pulls: Bt parts from the m-group (other a'), A parts from the n-group (other b')
-        self.pulls = []
-        si = 0
-        for a2 in range(pm):
-            if a2 == a:
-                continue
-            r = split(nb, pm, a2)
-            self.pulls.append(("Bt", self.owner[(a2, b, c)], r, si % 4, torch.cuda.Event()))
-            si += 1
-        for b2 in range(pn):
-            if b2 == b:
-                continue
-            r = split(mb, pn, b2)
-            self.pulls.append(("A", self.owner[(a, b2, c)], r, si % 4, torch.cuda.Event()))
-            si += 1
-        # one GEMM per destination in the k-group: the local destination first, written
-        # with plain (TMA) stores -- it initialises this GPU's rows of C, so C is never
-        # zeroed nor read back -- then, after a barrier, the peers' rows with TMA
-        # reduce-adds over NVLink
-        order = [(c + i) % pk for i in range(pk)]
-        self.gemms = [(split(mb, pk, d), self.owner[(a, b, d)]) for d in order]
+        # the schedule: pulls on one copy lane in need order, sub-products that wait
+        # only for what they read (plan_3d); the own rows of C first, written with plain
+        # (TMA) stores -- they initialise this GPU's rows, so C is never zeroed nor read
+        # back -- then, after a barrier, the peers' rows with TMA reduce-adds over NVLink
+        self.plan = plan_3d(self.grid, self.coord, self.owner, mb, nb)
+        self.pulls = self.plan["pulls"]
+        self.gemms = self.plan["gemms"]
         self.done = torch.cuda.Event()
         self.done.record()
         from ..peer import PeerBarrier
@@ -168,21 +224,22 @@ class MappedGemm3D:
             return progs[buf]
         prog = StepProgram()
         at = []
-        for name, q, (r0, r1), si, _ev in self.pulls:
+        for name, q, (r0, r1) in self.pulls:
             t = self.A if name == "A" else self.Bt
             pitch = t.shape[1] * 2
             off = r0 * pitch
             at.append(prog.pull(self.peers.ptrs[name][self.rank] + off, pitch,
-                                self.peers.ptrs[name][q] + off, pitch, pitch, r1 - r0,
-                                lane=si % 4))
-        for i in at:
-            prog.wait(i)
-        for i, ((r0, r1), dst) in enumerate(self.gemms):
-            if i == 1 and self._bar is not None:
+                                self.peers.ptrs[name][q] + off, pitch, pitch, r1 - r0, lane=0))
+        kb, nb = self.kb, self.nb
+        for i, ((r0, r1), (c0, c1), dst, d0, evs) in enumerate(self.gemms):
+            for e in evs:
+                prog.wait(at[e])
+            if i == self.plan["barrier_before"] and self._bar is not None:
                 prog.barrier(self._bar)  # every GPU has written its own rows of C[buf]
-            prog.gemm_bf16(self.A[r0:r1].data_ptr(), self.kb, self.Bt.data_ptr(), self.kb,
-                           self.peers.ptrs[f"C{buf}"][dst], self.nb, r1 - r0, self.nb, self.kb,
-                           0, 2 if i else 0)
+            prog.gemm_bf16(self.A.data_ptr() + r0 * kb * 2, kb,
+                           self.Bt.data_ptr() + c0 * kb * 2, kb,
+                           self.peers.ptrs[f"C{buf}"][dst] + ((r0 - d0) * nb + c0) * 4, nb,
+                           r1 - r0, c1 - c0, kb, 0, 0 if dst == self.rank else 2)
         progs[buf] = prog.build()
         return progs[buf]
 

@@ -171,7 +171,7 @@ class PanelPlan:
 
 
 def plan_panels(layout: Layout, me: int, K: int, mr: int, nc: int, block: int = 128,
-                a_chunks: int = 4, copy_streams: int = 4) -> PanelPlan:
+                a_chunks: int = 4, copy_streams: int = 1) -> PanelPlan:
     """The per-GPU SUMMA schedule (pure; CPU-testable).
 
     K is cut at every slice boundary of my row group (A) and column group (B),
@@ -293,7 +293,7 @@ class MappedGemm:
 
     def __init__(self, M: int, N: int, K: int, *, mapping: str = "decompose", rank: int = 0,
                  world: int = 1, group=None, block: int = 128, a_chunks: int = 4,
-                 seed: int = 0, out_dtype=None, copy_streams: int = 4):
+                 seed: int = 0, out_dtype=None, copy_streams: int = 1):
         torch = native.require_cuda()
         from ..gemm import tile_gemm  # noqa: F401  (fail early if the library is missing)
         from ..ownership import partition
