@@ -345,15 +345,19 @@ int pm_circuit_step(const pm_circuit_view* view, int32_t phase, void* stream);
  *   PM_STEP_GEMM_TF32     pm_gemm_tf32(src, lda, b, ldb, dst, ldc, m, n, k, accumulate);
  *   PM_STEP_MEMSET        zero `width` bytes at dst (compute stream);
  *   PM_STEP_BARRIER       pm_peer_barrier(barrier);
- *   PM_STEP_COPY_BARRIER  pm_peer_copy_barrier(barrier, copies, n_copies, ticket).
+ *   PM_STEP_COPY_BARRIER  pm_peer_copy_barrier(barrier, copies, n_copies, ticket);
+ *   PM_STEP_FORK          the lanes (re)start after everything queued so far on the
+ *                         compute stream (later lane pulls follow e.g. a GEMM that
+ *                         read the buffers they overwrite).
  * pm_steps_run: the lanes fork from `stream` at the first lane pull (after
- * everything already queued on it) and join back at the end of the step; no
+ * everything already queued on it) or at a PM_STEP_FORK, and join back at the end
+ * of the step; no
  * host synchronisation; capturable in a CUDA graph.  The program keeps its own
  * copy of the ops (and copy lists) but not of the memory they point to. */
 #define PM_STEP_LANES 4
 enum {
   PM_STEP_PULL = 0, PM_STEP_WAIT = 1, PM_STEP_GEMM_BF16 = 2, PM_STEP_GEMM_TF32 = 3,
-  PM_STEP_MEMSET = 4, PM_STEP_BARRIER = 5, PM_STEP_COPY_BARRIER = 6
+  PM_STEP_MEMSET = 4, PM_STEP_BARRIER = 5, PM_STEP_COPY_BARRIER = 6, PM_STEP_FORK = 7
 };
 typedef struct pm_step_op {
   int32_t kind, lane;

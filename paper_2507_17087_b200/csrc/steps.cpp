@@ -67,7 +67,7 @@ int pm_steps_create(const pm_step_op* ops, int32_t n, pm_steps** out) {
                                o.lane), PM_ERR_INVALID;
         }
         break;
-      case PM_STEP_GEMM_BF16: case PM_STEP_GEMM_TF32: case PM_STEP_MEMSET:
+      case PM_STEP_GEMM_BF16: case PM_STEP_GEMM_TF32: case PM_STEP_MEMSET: case PM_STEP_FORK:
         break;
       case PM_STEP_BARRIER:
         if (!o.barrier) {
@@ -163,6 +163,12 @@ int pm_steps_run(pm_steps* s, void* stream) {
       case PM_STEP_COPY_BARRIER:
         rc = pm_peer_copy_barrier(static_cast<const pm_peer_barrier_view*>(o.barrier), o.copies,
                                   o.n_copies, o.ticket, stream);
+        break;
+      case PM_STEP_FORK:  // later lane pulls follow everything queued so far on cs
+        PM_CUDA_TRY(cudaEventRecord(s->start, cs));
+        for (int l = 0; l < PM_STEP_LANES; ++l)
+          if (s->used[l]) PM_CUDA_TRY(cudaStreamWaitEvent(s->lanes[l], s->start, 0));
+        forked = true;
         break;
     }
     if (rc) return rc;

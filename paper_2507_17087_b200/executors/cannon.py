@@ -232,7 +232,17 @@ class MappedCannon:
         moved = 0
         first = True  # the first local product overwrites C (Cannon); 2.5D always adds
         pending = []  # a round's pulls, issued with its closing barrier (one launch)
-        for op in cannon_schedule(q, c, self.coord):
+        ops = cannon_schedule(q, c, self.coord)
+        if not self._fused_pulls and q > 1:
+            # copy engines: a round's shift pulls read the peers' current blocks (valid
+            # since the barrier that opened the round) into the other slot (not read by
+            # this round's GEMMs) -- hoist them ahead of the GEMMs onto a copy lane so
+            # the transfer overlaps the multiply; the round's barrier waits for them
+            self._build_overlapped(prog, ops, buf)
+            self.moved_blocks = sum(1 for op in ops if op[0] == "pull" and
+                                    self.owner[op[2]] != self.rank)
+            return prog.build()
+        for op in ops:
             if op[0] == "barrier":
                 if self._bar is not None and pending and self._fused_pulls:
                     prog.copy_barrier(self._bar, [(d, sp, w * h) for d, sp, w, h in pending])
@@ -266,6 +276,53 @@ class MappedCannon:
                 first = False
         self.moved_blocks = moved
         return prog.build()
+
+    def _gemm(self, prog, buf, slot, d, first):
+        """C(rows of layer d) += A[slot] B[slot], reduce-added into the owning layer."""
+        c = self.c
+        i, j, _ = self.coord
+        r0, r1 = split(self.nb, c, d)
+        cptr = self.peers.ptrs[f"C{buf}"][self.owner[(i, j, d)]]
+        a_blk, b_blk = self.A[slot], self.Bt[slot]
+        acc = 2 if c > 1 else int(not first)
+        if self.dtype == "fp32":
+            prog.gemm_tf32(a_blk[r0:r1].data_ptr(), self.nb, b_blk.data_ptr(), self.nb, cptr,
+                           self.nb, r1 - r0, self.nb, self.nb, acc)
+        else:
+            prog.gemm_bf16(a_blk[r0:r1].data_ptr(), self.nb, b_blk.data_ptr(), self.nb, cptr,
+                           self.nb, r1 - r0, self.nb, self.nb, 0, acc)
+
+    def _build_overlapped(self, prog, ops, buf):
+        """Copy-engine schedule with each round's shift pulls overlapping its GEMMs."""
+        rounds, cur = [], []
+        for op in ops:  # segments between barriers
+            if op[0] == "barrier":
+                rounds.append(cur)
+                cur = []
+            else:
+                cur.append(op)
+        rounds.append(cur)
+        first = True
+        for n, seg in enumerate(rounds):
+            if n:
+                if self._bar is not None:
+                    prog.barrier(self._bar)
+            pulls = [op for op in seg if op[0] == "pull"]
+            gemms = [op for op in seg if op[0] == "gemm"]
+            at = []
+            if pulls:
+                prog.fork()  # after the previous round's GEMMs (they read these slots)
+                for _, name, src, (kind, slot) in pulls:
+                    dst = self.A[slot] if kind == "A" else self.Bt[slot]
+                    w = self.nb * dst.element_size()
+                    at.append(prog.pull(dst.data_ptr(), w,
+                                        self.peers.ptrs[name][self.owner[src]], w, w, self.nb,
+                                        lane=0))
+            for _, slot, d in gemms:
+                self._gemm(prog, buf, slot, d, first)
+                first = False
+            for a in at:
+                prog.wait(a)
 
     def result(self):
         self._barrier()

@@ -125,7 +125,7 @@ class PmStepOp(ctypes.Structure):
                 ("n_copies", ctypes.c_int32), ("ticket", ctypes.c_void_p)]
 
 
-PULL, WAIT, GEMM_BF16, GEMM_TF32, MEMSET, BARRIER, COPY_BARRIER = range(7)
+PULL, WAIT, GEMM_BF16, GEMM_TF32, MEMSET, BARRIER, COPY_BARRIER, FORK = range(8)
 LANES = 4
 
 
@@ -133,8 +133,8 @@ class StepProgram:
     """One GPU's per-step schedule as data (csrc/steps.cpp, pm_steps_*): built once by
     an executor's planner over fixed device / peer pointers, replayed by one C call
     per step (`run`).  Ops: pull (copy-engine copy on a lane, or on the compute
-    stream with lane=-1), wait (the compute stream on a lane pull), GEMMs, memset,
-    peer barriers."""
+    stream with lane=-1), wait (the compute stream on a lane pull), fork (the lanes
+    restart after the compute stream's work so far), GEMMs, memset, peer barriers."""
 
     def __init__(self):
         self.ops = []
@@ -148,6 +148,10 @@ class StepProgram:
 
     def wait(self, pull_index: int) -> None:
         self.ops.append(PmStepOp(kind=WAIT, lane=pull_index))
+
+    def fork(self) -> None:
+        """Later lane pulls start after everything issued so far on the compute stream."""
+        self.ops.append(PmStepOp(kind=FORK))
 
     def gemm_bf16(self, A, lda, Bt, ldb, C, ldc, m, n, k, c_bf16=0, accumulate=0) -> None:
         self.ops.append(PmStepOp(kind=GEMM_BF16, src=A, lda=lda, b=Bt, ldb=ldb, dst=C, ldc=ldc,
