@@ -145,3 +145,24 @@ def test_ctypes_structs_match_the_header_layout():
         want = _c_layout(struct, [renames.get(n, n) for n in names])
         got = [ctypes.sizeof(cls)] + [getattr(cls, n).offset for n in names]
         assert got == want, (struct, list(zip(["sizeof"] + names, got, want)))
+
+
+def test_step_op_kinds_match_the_header():
+    """peer.py's step-op kinds are the header's PM_STEP_* values, and pm_steps_create
+    rejects an unknown kind before touching the GPU."""
+    import ctypes
+    import re
+
+    from paper_2507_17087_b200 import peer
+
+    hdr = (ROOT / "include" / "mapple_b200.h").read_text()
+    enum = dict((k, int(v)) for k, v in re.findall(r"PM_STEP_(\w+) = (\d+)", hdr))
+    for name in ("PULL", "WAIT", "GEMM_BF16", "GEMM_TF32", "MEMSET", "BARRIER",
+                 "COPY_BARRIER", "FORK"):
+        assert getattr(peer, name) == enum[name], name
+    assert peer.LANES == int(re.search(r"#define PM_STEP_LANES (\d+)", hdr).group(1))
+    lib = native.lib()
+    bad = (peer.PmStepOp * 1)(peer.PmStepOp(kind=99))
+    out = ctypes.c_void_p()
+    assert lib.pm_steps_create(bad, 1, ctypes.byref(out)) != 0
+    assert b"unknown kind" in lib.pm_last_error()
