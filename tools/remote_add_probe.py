@@ -30,7 +30,7 @@ def main():
         with torch.cuda.device(0):
             s = native.stream_ptr(torch.cuda.current_stream(0))
             seq = [("store_local", C0, 0), ("add_local", C0, 2), ("add_peer", C1, 2),
-                   ("acc_local", C0, 1)] * 3
+                   ("store_peer", C1, 0)] * 3
             for name, C, acc in seq:
                 for _ in range(2):
                     native.check(lib.pm_gemm_bf16(A.data_ptr(), K, Bt.data_ptr(), K, C.data_ptr(),
