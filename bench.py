@@ -800,6 +800,36 @@ def hot_path_kernels(args):
                                         "vs_k1_then_k2": (k1_ms + k2_ms) / k12_ms}}
 
 
+def cublas_same_shape(ex, rounds=3):
+    """cuBLAS (torch.matmul, bf16 in / bf16 out) beside K4 (bf16 in / fp32 out) on the same
+    32768^3 operands, interleaved launch by launch so both see the same clocks / power
+    state; median CUDA-event time of each."""
+    import torch
+
+    from paper_2507_17087_b200.gemm import tile_gemm
+
+    A, Bt, C = ex.A, ex.Bt, ex.C
+    out = torch.empty(A.shape[0], Bt.shape[0], dtype=torch.bfloat16, device=A.device)
+    ours, theirs = [], []
+    for _ in range(rounds):
+        for fn, acc in ((lambda: tile_gemm(A, Bt, C), ours),
+                        (lambda: torch.matmul(A, Bt.t(), out=out), theirs)):
+            fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            acc.append(e0.elapsed_time(e1))
+    flops = 2.0 * A.shape[0] * Bt.shape[0] * A.shape[1]
+    o, t = statistics.median(ours), statistics.median(theirs)
+    del out
+    return {"k4_ms": o, "k4_tflops": flops / (o * 1e-3) / 1e12, "cublas_ms": t,
+            "cublas_tflops": flops / (t * 1e-3) / 1e12, "k4_vs_cublas": t / o,
+            "note": "interleaved single launches on the headline operands; K4 writes fp32 C "
+                    "(4 GiB), cuBLAS bf16 C (2 GiB)"}
+
+
 def main_ours(args):
     import torch
 
@@ -807,6 +837,7 @@ def main_ours(args):
     burst, sustained, hbm, peak_src = peaks()
     ex, dec = run_mapping(args, rank, world, local, "decompose")
     e2e = run_e2e(args, ex, rank, world) if not args.no_e2e else None
+    cublas = cublas_same_shape(ex) if world == 1 and not args.no_kernels else None
     ex.close()
     del ex
     torch.cuda.empty_cache()
@@ -980,7 +1011,8 @@ def main_ours(args):
                      "power_capped": capped,
                      "kernel": "pm::gemm::wide::k_gemm_bf16_wide (tcgen05 cta_group::2, pair "
                                "tile 512x256, TMA ring, TMEM, dynamic tile scheduler)",
-                     "traffic": traffic},
+                     "traffic": traffic,
+                     "cublas_same_shape": cublas},
         "cpu_baseline": cpu,
         "clocks": dec["clocks"],
         "gpu_launches": dec["gemm_launches_per_step"] * args.steps,
