@@ -260,7 +260,8 @@ int stable_partition_small(Key key, Sink sink, bool scatter, long long n, int nb
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
   bool per_warp = false;
   if constexpr (Key::kVec4 && Key::kRaw4) {
-    per_warp = !getenv("PM_HIST_CTA");
+    static const bool cta_per_tile = getenv("PM_HIST_CTA") != nullptr;  // A/B knob
+    per_warp = !cta_per_tile;
     if (per_warp)
       k_small_hist_warp<Key><<<(unsigned)((ntiles + kPartWarps - 1) / kPartWarps), kPartThreads,
                                smem_h, s>>>(key, n, nbins, ntiles, hist);
