@@ -50,3 +50,30 @@ def test_partition_rejects_bad_ids(cuda):
         partition(ids, 8)
     empty = partition(torch.zeros(0, dtype=torch.int32, device="cuda"), 4)
     assert empty.counts.tolist() == [0, 0, 0, 0]
+
+
+@pytest.mark.parametrize("n", [4096 * 300 + 17, 10_000_003])
+def test_partition_block_ids_uniform_tiles(cuda, n):
+    """Block-structured ids (the mapped-launch case: most 4096-id tiles hold one
+    processor, so the scatter writes them as runs and the warp-per-tile histogram
+    classifies them) mixed with a random stretch, also through an unaligned view (no
+    16-byte loads), against a stable sort."""
+    torch = cuda
+    nbins = 8
+    ids = (torch.arange(n, device="cuda", dtype=torch.int64) * nbins // n).to(torch.int32)
+    g = torch.Generator(device="cuda").manual_seed(n)
+    ids[n // 3: n // 3 + 50_000] = torch.randint(0, nbins, (50_000,), device="cuda",
+                                                 dtype=torch.int32, generator=g)
+    for view in (ids, ids[1:]):
+        own = partition(view, nbins)
+        assert torch.equal(own.counts, torch.bincount(view.long(), minlength=nbins))
+        assert torch.equal(own.perm, torch.sort(view, stable=True).indices.to(torch.int32))
+
+
+def test_partition_flags_bad_id_in_uniform_region(cuda):
+    torch = cuda
+    n = 4096 * 64
+    ids = (torch.arange(n, device="cuda", dtype=torch.int64) * 4 // n).to(torch.int32)
+    ids[4096 * 10 + 123] = -3  # inside an otherwise uniform tile: the vector path checks it
+    with pytest.raises(ProcMapError):
+        partition(ids, 4)
