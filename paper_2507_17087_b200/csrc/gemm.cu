@@ -1229,7 +1229,13 @@ extern "C" int pm_gemm_bf16(const void* A, int64_t lda, const void* Bt, int64_t 
   // (reduce-adding launches -- C in a peer's memory -- measured the same with and without
   // it, and with half a wave of slack: Johnson (1,1,2) / (1,2,2) within +-2% run to run,
   // tools/grid3d_ab2.sh)
-  const bool wave = kind == 2 && !(getenv("PM_GEMM_WAVESYNC") && atoi(getenv("PM_GEMM_WAVESYNC")) == 0);
+  // Not for reduce-adding launches (C in a peer's memory: the 3-D / 2.5D fused
+  // reduce-scatter): wave-aligned tiles would all drain over NVLink at once -- interleaved
+  // single launches into a peer, 16384^3 6.76 -> 6.32 ms and 16384x32768x16384 13.34 ->
+  // 12.71 ms without it (tools/remote_add_probe.py); PM_GEMM_ADD_WAVE=1 keeps it
+  static const bool add_wave = getenv("PM_GEMM_ADD_WAVE") != nullptr;
+  const bool wave = kind == 2 && (!atomic_add || add_wave) &&
+                    !(getenv("PM_GEMM_WAVESYNC") && atoi(getenv("PM_GEMM_WAVESYNC")) == 0);
   p.group_m = kind == 2 ? (wave ? 4 : (K >= 24576 ? 2 : 4)) : 8;
   if (const char* g = getenv("PM_GEMM_GROUP")) p.group_m = atoi(g) > 0 ? atoi(g) : p.group_m;
   p.debug_nostore = getenv("PM_GEMM_NOSTORE") ? 1 : 0;

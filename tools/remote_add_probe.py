@@ -30,8 +30,13 @@ def main():
         with torch.cuda.device(0):
             s = native.stream_ptr(torch.cuda.current_stream(0))
             seq = [("store_local", C0, 0), ("add_local", C0, 2), ("add_peer", C1, 2),
-                   ("store_peer", C1, 0)] * 3
+                   ("add_peer_nowave", C1, 2)] * 4
+            import os
             for name, C, acc in seq:
+                if name.endswith("_nowave"):
+                    os.environ["PM_GEMM_WAVESYNC"] = "0"
+                else:
+                    os.environ.pop("PM_GEMM_WAVESYNC", None)
                 for _ in range(2):
                     native.check(lib.pm_gemm_bf16(A.data_ptr(), K, Bt.data_ptr(), K, C.data_ptr(),
                                                   N, M, N, K, 0, acc, s), "gemm")
