@@ -253,37 +253,49 @@ def run_mapping(args, rank, world, local, mapping, mnk=None):
     return ex, res
 
 
-def run_3d(args, rank, world, local, M, N, K, mapping):
-    """Time one 3-D mapped multiply (Johnson / COSMA grid) with the fused
-    GEMM + NVLink reduce-scatter; max over ranks of CUDA-event time."""
+def run_3d_pair(args, rank, world, local, M, N, K, rounds=3):
+    """Time one 3-D mapped multiply (Johnson / COSMA grid, fused GEMM + NVLink
+    reduce-scatter) under the decompose AND the heuristic mapping: both executors live at
+    once and their timed blocks alternate `rounds` times (the box's power state drifts by
+    several % over a run, so back-to-back blocks would favour whichever runs first);
+    per mapping the median block, each block's time the max over ranks of CUDA events."""
     import torch
 
     from paper_2507_17087_b200.executors.grid3d import MappedGemm3D
 
-    ex = MappedGemm3D(M, N, K, mapping=mapping, rank=rank, world=world, seed=99)
     cs = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        ex.step()
-    ex.result()
-    torch.cuda.synchronize()
-    barrier(world)
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     steps = max(3, args.steps // 2)
-    t0.record(cs)
-    for _ in range(steps):
-        ex.step()
-    ex.result()  # the last step's reduce-adds from the peers have landed
-    t1.record(cs)
-    torch.cuda.synchronize()
-    ms = max_over_ranks(t0.elapsed_time(t1) / steps, world)
-    res = {"grid": list(ex.grid), "ms_per_step": ms,
-           "tflops": 2.0 * M * N * K / (ms * 1e-3) / 1e12,
-           "comm_bytes_per_gpu": ex.comm, "steps": steps,
-           "gpu_launches_per_step": ex.gemm_launches}
-    ex.close()
-    del ex
+    exs = {m: MappedGemm3D(M, N, K, mapping=m, rank=rank, world=world, seed=99)
+           for m in ("decompose", "heuristic")}
+    for ex in exs.values():
+        for _ in range(args.warmup):
+            ex.step()
+        ex.result()
+    times = {m: [] for m in exs}
+    for _ in range(rounds):
+        for m, ex in exs.items():
+            torch.cuda.synchronize()
+            barrier(world)
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record(cs)
+            for _ in range(steps):
+                ex.step()
+            ex.result()  # the last step's reduce-adds from the peers have landed
+            t1.record(cs)
+            torch.cuda.synchronize()
+            times[m].append(max_over_ranks(t0.elapsed_time(t1) / steps, world))
+    out = {}
+    for m, ex in exs.items():
+        ms = statistics.median(times[m])
+        out[m] = {"grid": list(ex.grid), "ms_per_step": ms,
+                  "tflops": 2.0 * M * N * K / (ms * 1e-3) / 1e12,
+                  "ms_per_step_blocks": times[m],
+                  "comm_bytes_per_gpu": ex.comm, "steps": steps, "rounds": rounds,
+                  "gpu_launches_per_step": ex.gemm_launches}
+        ex.close()
+    del exs
     torch.cuda.empty_cache()
-    return res
+    return out["decompose"], out["heuristic"]
 
 
 def run_cannon(args, rank, world, N, layers, dtype, graph=False):
@@ -878,8 +890,7 @@ def main_ours(args):
             wl = {}
             for name, (M, N, K) in (("johnson3d", (args.size,) * 3),
                                     ("cosma", (2 * args.size, args.size // 2, args.size // 2))):
-                d = run_3d(args, rank, world, local, M, N, K, "decompose")
-                h = run_3d(args, rank, world, local, M, N, K, "heuristic")
+                d, h = run_3d_pair(args, rank, world, local, M, N, K)
                 wl[name] = {"M": M, "N": N, "K": K, "decompose": d, "heuristic": h,
                             "speedup": d["tflops"] / h["tflops"],
                             "comm_ratio": h["comm_bytes_per_gpu"]["total"] /
