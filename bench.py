@@ -298,6 +298,45 @@ def run_3d_pair(args, rank, world, local, M, N, K, rounds=3):
     return out["decompose"], out["heuristic"]
 
 
+def run_2d_pair(args, rank, world, M, N, K, rounds=3):
+    """SUMMA / PUMMA panels under both mappings, timed in alternating blocks (as
+    run_3d_pair); per mapping the median block, max over ranks."""
+    import torch
+
+    from paper_2507_17087_b200.executors.summa import MappedGemm
+
+    cs = torch.cuda.current_stream()
+    exs = {m: MappedGemm(M, N, K, mapping=m, rank=rank, world=world, a_chunks=args.chunks,
+                         seed=1234) for m in ("decompose", "heuristic")}
+    for ex in exs.values():
+        for _ in range(args.warmup):
+            ex.step()
+    times = {m: [] for m in exs}
+    for _ in range(rounds):
+        for m, ex in exs.items():
+            torch.cuda.synchronize()
+            barrier(world)
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record(cs)
+            for _ in range(args.steps):
+                ex.step()
+            t1.record(cs)
+            torch.cuda.synchronize()
+            times[m].append(max_over_ranks(t0.elapsed_time(t1) / args.steps, world))
+    out = {}
+    for m, ex in exs.items():
+        ms = statistics.median(times[m])
+        out[m] = {"grid": list(ex.layout.grid), "ms_per_step": ms,
+                  "tflops": 2.0 * M * N * K / (ms * 1e-3) / 1e12, "ms_per_step_blocks": times[m],
+                  "comm_bytes_per_gpu_max": int(max_over_ranks(ex.recv_bytes, world)),
+                  "comm_bytes_total": int(sum_over_ranks(ex.recv_bytes, world)),
+                  "gemm_launches_per_step": ex.gemm_launches, "rounds": rounds}
+        ex.close()
+    del exs
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_cannon(args, rank, world, N, layers, dtype, graph=False):
     """BASELINE configs[0] (Cannon fp32 N=1024 on 2x2) and the Cannon / 2.5D
     bf16 variants: Cannon skew + shifts as NVLink pulls, 2.5D layer reduction
@@ -903,14 +942,7 @@ def main_ours(args):
             # where the decompose grid differs from Algorithm 1's (e.g. (4,1) vs (2,2))
             mnk = (2 * args.size, args.size // 2, args.size // 2)
             out = {"M": mnk[0], "N": mnk[1], "K": mnk[2]}
-            for mapping in ("decompose", "heuristic"):
-                ex, r = run_mapping(args, rank, world, local, mapping, mnk)
-                ex.close()
-                del ex
-                torch.cuda.empty_cache()
-                out[mapping] = {k: r[k] for k in ("grid", "ms_per_step", "tflops",
-                                                  "comm_bytes_per_gpu_max", "comm_bytes_total",
-                                                  "gemm_launches_per_step")}
+            out.update(run_2d_pair(args, rank, world, *mnk))
             out["speedup"] = out["decompose"]["tflops"] / out["heuristic"]["tflops"]
             out["comm_ratio"] = (out["heuristic"]["comm_bytes_total"] /
                                  max(1, out["decompose"]["comm_bytes_total"]))
