@@ -586,13 +586,12 @@ def run_e2e_pipelined_multi(args, ex, rank, world):
 
     from paper_2507_17087_b200.executors.summa import MappedGemm
 
-    lay = ex.layout
-    ka, kb = lay.a_slice[rank], lay.b_slice[rank]
     ex2 = MappedGemm(ex.M, ex.N, ex.K, mapping=ex.mapping, rank=rank, world=world,
                      a_chunks=args.chunks)
     sets = [ex, ex2]
-    hA = ex.A[:, ka[0]:ka[1]].contiguous().cpu().pin_memory()
-    hB = ex.Bt[:, kb[0]:kb[1]].contiguous().cpu().pin_memory()
+    # this GPU's own slices in its K-rotated buffers: 1 or 2 column pieces each
+    hA = [ex.A[:, p0:p0 + n].contiguous().cpu().pin_memory() for p0, _, n in ex.own_a]
+    hB = [ex.Bt[:, p0:p0 + n].contiguous().cpu().pin_memory() for p0, _, n in ex.own_b]
     hC = [torch.empty(ex.C.shape, dtype=ex.C.dtype).pin_memory() for _ in range(2)]
     cs = torch.cuda.current_stream()
     h2d, d2h, comm = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
@@ -621,8 +620,10 @@ def run_e2e_pipelined_multi(args, ex, rank, world):
             h2d.wait_event(ev["free"][b])      # every GPU done pulling from set b
             mark(h2d)
             with torch.cuda.stream(h2d):
-                E.A[:, ka[0]:ka[1]].copy_(hA, non_blocking=True)
-                E.Bt[:, kb[0]:kb[1]].copy_(hB, non_blocking=True)
+                for (p0, _, n), h in zip(E.own_a, hA):
+                    E.A[:, p0:p0 + n].copy_(h, non_blocking=True)
+                for (p0, _, n), h in zip(E.own_b, hB):
+                    E.Bt[:, p0:p0 + n].copy_(h, non_blocking=True)
             ev["in"][b].record(h2d)
             mark(h2d)
             comm.wait_event(ev["in"][b])
@@ -663,7 +664,7 @@ def run_e2e_pipelined_multi(args, ex, rank, world):
     ex2.close()
     del ex2
     torch.cuda.empty_cache()
-    h2d_b = sum_over_ranks(hA.numel() * 2 + hB.numel() * 2, world)
+    h2d_b = sum_over_ranks(sum(h.numel() * 2 for h in hA + hB), world)
     d2h_b = sum_over_ranks(hC[0].numel() * hC[0].element_size(), world)
     S = args.size
     return {"value": 2 * S ** 3 / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,

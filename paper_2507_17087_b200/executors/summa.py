@@ -165,9 +165,11 @@ def synth_f32(rows: tuple, cols: tuple, ld: int, seed: int, device):
 class PanelPlan:
     panels: list      # (k0, k1, A source rank, B source rank), in execution order
     chunks: list      # A row chunks of remote panels
-    pulls: list       # (operand, source rank, row0, rows, k0, k1, stream index)
+    pulls: list       # (operand, source rank, row0, rows, k0, k1, stream index); k in
+                      # this GPU's rotated buffer positions (as the gemms' k0, k1)
     gemms: list       # (r0, r1, k0, k1, accumulate, [indices into pulls to wait for], c0, c1)
     n_streams: int
+    rot: int = 0      # K rotation of this GPU's A / Bt buffers: global k sits at (k - rot) % K
 
 
 def plan_panels(layout: Layout, me: int, K: int, mr: int, nc: int, block: int = 128,
@@ -213,6 +215,14 @@ def plan_panels(layout: Layout, me: int, K: int, mr: int, nc: int, block: int = 
         for r in sorted(ranked[1:], key=lambda r: -r[1]):
             if r[0] == 0 and r[2] == head[0][1]:
                 head.insert(0, r)
+    # K rotation: this GPU stores global k at buffer position (k - rot) % K with rot = the
+    # head's first K, so the head sits at [0, h) and everything after it is ONE contiguous
+    # range -- the remaining panels merge into as few runs (launches) as adjacency allows
+    # (the K order of a product's terms is free).  Panels never wrap: rot is a cut.
+    rot = head[0][1]
+    rp = lambda r: (r[0], (r[1] - rot) % K, (r[1] - rot) % K + (r[2] - r[1]), r[3], r[4])  # noqa: E731
+    head = [rp(r) for r in head]
+    ranked = [rp(r) for r in ranked]
     runs = []
     for r in sorted((r for r in ranked if r not in head), key=lambda r: r[1]):
         if runs and runs[-1][-1][2] == r[1]:
@@ -284,8 +294,19 @@ def plan_panels(layout: Layout, me: int, K: int, mr: int, nc: int, block: int = 
             b_evs = []  # later chunks of this run follow the first on one stream
         first = False
     ranked = [r for run in runs for r in run]
-    return PanelPlan([(k0, k1, a, b) for _, k0, k1, a, b in ranked], chunks, pulls, gemms,
-                     n_streams)
+    return PanelPlan([((k0 + rot) % K, (k0 + rot) % K + (k1 - k0), a, b)
+                      for _, k0, k1, a, b in ranked], chunks, pulls, gemms, n_streams, rot)
+
+
+def rotated_segments(k0: int, k1: int, rot: int, K: int) -> list:
+    """Global K range [k0, k1) -> [(buffer position, global k, length)] in a buffer rotated
+    by `rot` (1 piece, or 2 when the range crosses the rotation point)."""
+    p0 = (k0 - rot) % K
+    n = k1 - k0
+    if p0 + n <= K:
+        return [(p0, k0, n)]
+    first = K - p0
+    return [(p0, k0, first), (0, k0 + first, n - first)]
 
 
 class MappedGemm:
@@ -315,13 +336,23 @@ class MappedGemm:
         rc = self.layout.rects[rank]
         self.rows, self.cols = (rc.r0, rc.r1), (rc.c0, rc.c1)
         mr, nc = rc.r1 - rc.r0, rc.c1 - rc.c0
-        # 3: operand buffers with full K; this GPU's own slices live in place
+        # 3: operand buffers with full K, K-rotated per GPU (plan_panels: global k at
+        # (k - rot) % K); this GPU's own slices live in place
+        mrs = [(r.r1 - r.r0, r.c1 - r.c0) for r in self.layout.rects]
+        self.rots = [plan_panels(self.layout, q, K, mrs[q][0], mrs[q][1], block, a_chunks,
+                                 copy_streams).rot for q in range(world)]
+        rot = self.rots[rank]
         self.A = torch.empty(mr, K, dtype=torch.bfloat16, device=self.device)
         self.Bt = torch.empty(nc, K, dtype=torch.bfloat16, device=self.device)
         self.C = torch.empty(mr, nc, dtype=out_dtype or torch.float32, device=self.device)
         ka, kb = self.layout.a_slice[rank], self.layout.b_slice[rank]
-        self.A[:, ka[0]:ka[1]] = synth(self.rows, ka, K, seed, self.device)
-        self.Bt[:, kb[0]:kb[1]] = synth(self.cols, kb, K, seed + 1, self.device)
+        # own slices as (buffer position, global k, length) pieces
+        self.own_a = rotated_segments(ka[0], ka[1], rot, K)
+        self.own_b = rotated_segments(kb[0], kb[1], rot, K)
+        for p0, k0, n in self.own_a:
+            self.A[:, p0:p0 + n] = synth(self.rows, (k0, k0 + n), K, seed, self.device)
+        for p0, k0, n in self.own_b:
+            self.Bt[:, p0:p0 + n] = synth(self.cols, (k0, k0 + n), K, seed + 1, self.device)
         # the own slices are complete before any peer can learn their address (the
         # handle exchange is collective): a peer's first pull never reads them early
         torch.cuda.synchronize(self.device)
@@ -351,14 +382,26 @@ class MappedGemm:
 
     # -- one multiply ---------------------------------------------------------------
 
+    def _pieces(self, q, k0, k1):
+        """A pull of my buffer positions [k0, k1) (one panel: a global K range that does not
+        wrap) from GPU q, which stores global k at its own rotation: [(my position, q's
+        position, length)], 1 piece or 2 when the range crosses q's rotation point."""
+        K, rm = self.K, self.rots[self.rank]
+        g0 = (k0 + rm) % K
+        if g0 + (k1 - k0) > K:
+            raise AssertionError("a pulled panel crossed the end of K")
+        return [((gk - rm) % K, pq, n)
+                for pq, gk, n in rotated_segments(g0, g0 + (k1 - k0), self.rots[q], K)]
+
     def _copy(self, name, q, row0, nrows, k0, k1, stream):
         from ..peer import copy2d
 
         esz = 2
         pitch = self.K * esz
-        src = self.peers.ptrs[name][q] + (row0 * self.K + k0) * esz
-        dst = self.peers.ptrs[name][self.rank] + (row0 * self.K + k0) * esz
-        copy2d(dst, pitch, src, pitch, (k1 - k0) * esz, nrows, stream)
+        for pm, pq, n in self._pieces(q, k0, k1):
+            src = self.peers.ptrs[name][q] + (row0 * self.K + pq) * esz
+            dst = self.peers.ptrs[name][self.rank] + (row0 * self.K + pm) * esz
+            copy2d(dst, pitch, src, pitch, n * esz, nrows, stream)
 
     def _program(self):
         """The step as a StepProgram (csrc/steps.cpp): the same pulls on the same copy
@@ -376,16 +419,19 @@ class MappedGemm:
         pitch = K * esz
         at = {}
         for i, (name, q, row0, rows, k0, k1, si, _ev) in enumerate(self.pulls):
-            src = self.peers.ptrs[name][q] + (row0 * K + k0) * esz
-            dst = (self.A if name == "A" else self.Bt).data_ptr() + (row0 * K + k0) * esz
-            at[i] = prog.pull(dst, pitch, src, pitch, (k1 - k0) * esz, rows, lane=si % 4)
+            at[i] = []
+            for pm, pq, n in self._pieces(q, k0, k1):
+                src = self.peers.ptrs[name][q] + (row0 * K + pq) * esz
+                dst = (self.A if name == "A" else self.Bt).data_ptr() + (row0 * K + pm) * esz
+                at[i].append(prog.pull(dst, pitch, src, pitch, n * esz, rows, lane=si % 4))
         ev_index = {id(p[-1]): i for i, p in enumerate(self.pulls)}
         c_bf16 = int(self.C.dtype != native.require_cuda().float32)
         csz = self.C.element_size()
         nc = self.C.shape[1]
         for r0, r1, k0, k1, acc, evs, c0, c1 in self.gemms:
             for ev in evs:
-                prog.wait(at[ev_index[id(ev)]])
+                for a in at[ev_index[id(ev)]]:
+                    prog.wait(a)
             prog.gemm_bf16(self.A.data_ptr() + (r0 * K + k0) * esz, K,
                            self.Bt.data_ptr() + (c0 * K + k0) * esz, K,
                            self.C.data_ptr() + (r0 * nc + c0) * csz, nc, r1 - r0, c1 - c0,

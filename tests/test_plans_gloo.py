@@ -63,7 +63,8 @@ def _worker(rank, world, port, out_q):
                     # every pull names the GPU that holds that slice
                     for name, src, row0, rows, k0, k1, _ in plan.pulls:
                         sl = lay.a_slice[src] if name == "A" else lay.b_slice[src]
-                        assert sl[0] <= k0 and k1 <= sl[1] and src != r
+                        g0 = (k0 + plan.rot) % K  # pulls are in the rotated buffer's k
+                        assert sl[0] <= g0 and g0 + (k1 - k0) <= sl[1] and src != r
                         grp = lay.row_group[r] if name == "A" else lay.col_group[r]
                         assert src in grp
                     # bytes pulled == closed form 2[(M/pr)K(1-1/pc) + K(N/pc)(1-1/pr)]
